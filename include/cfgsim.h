@@ -1,0 +1,146 @@
+/*
+ * cfgsim — B200-native IsoRank CFG-pair similarity (C ABI).
+ *
+ * Drop-in boundary for the reference's ISO measure path
+ * (/root/reference/pkg/src/sasscfg, pure Python).  The reference has no FFI
+ * layer; each entry point below replaces the Python function cited, and the
+ * Python package paper_1707_02423_b200 binds them with ctypes
+ * (INTEGRATION.md shows the binding a sasscfg maintainer would add).
+ *
+ * Conventions
+ *  - every function returns int status (CFGSIM_OK == 0); no C++ exception
+ *    crosses the ABI; cfgsim_last_error() returns a thread-local message.
+ *  - plain pointers and sizes only.  Arrays marked [host|device] may be
+ *    either; the library detects device pointers (cudaPointerGetAttributes)
+ *    and stages host arrays itself.  Calls that touch a host output
+ *    synchronise the stream before returning; all-device calls are
+ *    stream-ordered and asynchronous.
+ *  - results are bitwise deterministic: independent of stream, launch
+ *    order, tile, grid size or device count.
+ *
+ * Packed corpus (CSR of the raw TransitionMatrix.entries, matrix.py:24-42):
+ *  graph g has n_nodes[g] rows; its row pointer is
+ *  rowptr[rp_off[g] .. rp_off[g] + n_nodes[g]] (local, starts at 0); its
+ *  column indices / values are col[nz_off[g] + e], val[nz_off[g] + e].
+ *  Values must be finite and >= 0 (matrix.py:35-36).
+ */
+#ifndef CFGSIM_H
+#define CFGSIM_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CFGSIM_API __attribute__((visibility("default")))
+#else
+#define CFGSIM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CFGSIM_OK 0
+#define CFGSIM_ERR_ARG 1      /* bad argument (reference: ValueError)          */
+#define CFGSIM_ERR_DIM 2      /* unequal sizes (reference: DimMismatch)         */
+#define CFGSIM_ERR_CUDA 3     /* CUDA runtime / launch failure                  */
+#define CFGSIM_ERR_NOMEM 4    /* device allocation failed                       */
+#define CFGSIM_ERR_NODEVICE 5 /* no usable sm_100 device: there is no CPU path  */
+
+#define CFGSIM_FP64 0
+#define CFGSIM_FP32 1
+
+typedef struct cfgsim_corpus cfgsim_corpus;
+
+/* alpha/tol/max_iter as isorank_align (similarity.py:111-118, defaults
+ * 0.85/1e-9/1000, corpus.py:86-88).  precision: CFGSIM_FP64 reproduces the
+ * reference (fp64); CFGSIM_FP32 iterates in fp32 and stops on
+ * delta < max(tol, tol_fp32) (fp32 cannot reach 1e-9). */
+typedef struct {
+  double alpha;
+  double tol;
+  int32_t max_iter;
+  int32_t precision;
+  double tol_fp32;
+} cfgsim_params;
+
+CFGSIM_API const char *cfgsim_last_error(void);
+CFGSIM_API int cfgsim_version(void);
+/* Number of sm_100 devices visible; 0 if none (callers must then fail). */
+CFGSIM_API int cfgsim_device_count(int32_t *n);
+
+/* Pack + upload a corpus to `device` (replaces the list[TransitionMatrix]
+ * that pairwise() walks, similarity.py:229).  Graphs are also ordered by
+ * node count internally (tier bucketing). */
+CFGSIM_API int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
+                         const int64_t *rp_off, const int32_t *rowptr, const int64_t *nz_off,
+                         const int32_t *col, const double *val, cfgsim_corpus **out);
+CFGSIM_API int cfgsim_corpus_destroy(cfgsim_corpus *c);
+CFGSIM_API int cfgsim_corpus_info(const cfgsim_corpus *c, int32_t *n_graphs, int32_t *max_nodes,
+                       int64_t *device_bytes);
+
+/* measure_distance(A[ia[p]], B[ib[p]], MeasureId.ISO) for p < n_pairs
+ * (similarity.py:176-189: normalize_pair -> isorank_align ->
+ * isorank_distance).  Outputs d (distance in [1,2]), W (matched weight,
+ * similarity.py:150), iters, converged; any output may be NULL.
+ * A and B must live on the same device.  [host|device] arrays. */
+CFGSIM_API int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_pairs,
+                         const int32_t *ia, const int32_t *ib, const cfgsim_params *p,
+                         double *d, double *W, int32_t *iters, uint8_t *converged,
+                         void *cuda_stream);
+
+/* All-pairs over one corpus (pairwise(..., MeasureId.ISO), similarity.py:211-246).
+ * Work is the upper triangle in size-sorted order: n_units =
+ * K(K+1)/2 unordered pairs {i <= j}.  ordered == 0: one alignment per unit,
+ * d(j,i) := d(i,j) (ISO symmetry).  ordered == 1: both
+ * directions computed separately exactly like the reference's double loop.
+ * cfgsim_allpairs_units  -> number of units.
+ * cfgsim_allpairs_split  -> world+1 cost-balanced unit boundaries (for
+ *                           row-free sharding across GPUs).
+ * cfgsim_allpairs_range  -> computes units [u0,u1) into unit-linear outputs
+ *                           d_lin/iters_lin ((u1-u0) entries, x2 when ordered;
+ *                           [device]).
+ * cfgsim_allpairs_scatter-> scatters a full unit-linear vector (all units)
+ *                           into the K x K row-major matrix in the caller's
+ *                           graph order, both triangles [device].
+ * cfgsim_allpairs        -> convenience: range(all) + scatter, [host|device]
+ *                           K x K outputs (iters_mat may be NULL). */
+CFGSIM_API int cfgsim_allpairs_units(const cfgsim_corpus *c, int64_t *n_units);
+CFGSIM_API int cfgsim_allpairs_split(const cfgsim_corpus *c, int32_t world, int64_t *bounds);
+CFGSIM_API int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_t ordered,
+                          const cfgsim_params *p, double *d_lin, int32_t *iters_lin,
+                          void *cuda_stream);
+CFGSIM_API int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const double *d_lin,
+                            const int32_t *iters_lin, double *d_mat, int32_t *iters_mat,
+                            void *cuda_stream);
+CFGSIM_API int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params *p,
+                    double *d_mat, int32_t *iters_mat, void *cuda_stream);
+
+/* One alignment with full outputs: isorank_align(a, b, alpha, tol, max_iter,
+ * start) (similarity.py:111-157) after normalize_pair.  A (na x na), B
+ * (nb x nb) dense row-major host arrays; x0 = start/sum(start) (N*N) or
+ * NULL; X_out (N*N) and match_out (N) may be NULL.  N = max(na, nb). */
+CFGSIM_API int cfgsim_isorank_single(int32_t device, int32_t na, const double *A, int32_t nb,
+                          const double *B, const cfgsim_params *p, const double *x0,
+                          double *X_out, int32_t *match_out, double *d, double *W,
+                          int32_t *iters, uint8_t *converged);
+
+/* Query-vs-corpus best match: for each query q, argmin_j d(Q[q], C[j]) over
+ * j in [c0, c1) with ties to the lowest j (np.argmin over a pairwise row).
+ * best_idx is the corpus index.  [host|device] outputs. */
+CFGSIM_API int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, int32_t c1,
+                   const cfgsim_params *p, double *best_d, int64_t *best_idx,
+                   void *cuda_stream);
+
+/* interpolate_to(m, target) (matrix.py:74-106), bit-exact, on the device.
+ * src n x n, dst target x target, dense row-major host arrays. */
+CFGSIM_API int cfgsim_interpolate(int32_t device, int32_t n, const double *src, int32_t target,
+                       double *dst);
+
+/* Number of pair-kernel launches issued by this process so far (bench
+ * evidence for gpu_launches). */
+CFGSIM_API int64_t cfgsim_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFGSIM_H */

@@ -1,0 +1,114 @@
+"""ctypes binding of the sm_100a C-ABI library ``libcfgsim.so`` (include/cfgsim.h).
+
+The library is built in-tree by ``__graft_entry__.build()``
+(``csrc/Makefile``).  There is no CPU fallback: if the library is missing
+this module raises on import, and every compute entry point raises
+``DeviceError`` when no sm_100 GPU is visible.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import DeviceError, DimMismatch
+
+LIB_PATH = Path(__file__).resolve().parent / "libcfgsim.so"
+
+OK, ERR_ARG, ERR_DIM, ERR_CUDA, ERR_NOMEM, ERR_NODEVICE = range(6)
+FP64, FP32 = 0, 1
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the IsoRank path runs only on sm_100a; there is no CPU fallback)"
+    )
+
+lib = C.CDLL(str(LIB_PATH))
+
+
+class Params(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("tol", C.c_double), ("max_iter", C.c_int32),
+                ("precision", C.c_int32), ("tol_fp32", C.c_double)]
+
+
+_vp = C.c_void_p
+_i32 = C.c_int32
+_i64 = C.c_int64
+_pp = C.POINTER(Params)
+
+_SIGS = {
+    "cfgsim_last_error": ([], C.c_char_p),
+    "cfgsim_version": ([], C.c_int),
+    "cfgsim_device_count": ([_vp], C.c_int),
+    "cfgsim_corpus_create": ([_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
+    "cfgsim_corpus_destroy": ([_vp], C.c_int),
+    "cfgsim_corpus_info": ([_vp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_isorank_pairs": ([_vp, _vp, _i64, _vp, _vp, _pp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_allpairs_units": ([_vp, _vp], C.c_int),
+    "cfgsim_allpairs_split": ([_vp, _i32, _vp], C.c_int),
+    "cfgsim_allpairs_range": ([_vp, _i64, _i64, _i32, _pp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_allpairs_scatter": ([_vp, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_allpairs": ([_vp, _i32, _pp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_isorank_single": ([_i32, _i32, _vp, _i32, _vp, _pp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                              C.c_int),
+    "cfgsim_nearest": ([_vp, _vp, _i32, _i32, _pp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_interpolate": ([_i32, _i32, _vp, _i32, _vp], C.c_int),
+    "cfgsim_launch_count": ([], C.c_int64),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = (lib.cfgsim_last_error() or b"").decode(errors="replace")
+    if rc == ERR_ARG:
+        raise ValueError(msg)
+    if rc == ERR_DIM:
+        raise DimMismatch(msg)
+    if rc == ERR_NOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+def ptr(a) -> int | None:
+    """Raw address of a numpy array or torch tensor (None for None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if isinstance(a, int):
+        return a
+    raise TypeError(f"cannot take the address of {type(a)!r}")
+
+
+def params(alpha=0.85, tol=1e-9, max_iter=1000, precision="fp64", tol_fp32=1e-7) -> Params:
+    if precision not in ("fp64", "fp32"):
+        raise ValueError(f"precision must be 'fp64' or 'fp32', got {precision!r}")
+    return Params(float(alpha), float(tol), int(max_iter), FP64 if precision == "fp64" else FP32,
+                  float(tol_fp32))
+
+
+def device_count() -> int:
+    n = np.zeros(1, np.int32)
+    check(lib.cfgsim_device_count(ptr(n)))
+    return int(n[0])
+
+
+def default_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0")) if device_count() > 1 else 0
+
+
+def launch_count() -> int:
+    return int(lib.cfgsim_launch_count())

@@ -1,0 +1,108 @@
+"""CFG batching layer: pack transition matrices into CSR and keep them on the GPU.
+
+Replaces the reference's ``list[TransitionMatrix]`` walked pair by pair
+(``similarity.py:229-246``).  A corpus is packed once on the host
+(``pack``), uploaded once per device (``DeviceCorpus``), and then every
+all-pairs / query launch reads it from HBM.  The raw ``entries`` are packed
+(not the row-normalised operator): bilinear size normalisation depends on
+the partner's size, so it happens per pair inside the kernel prologue.
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as nat
+
+
+def _entries(m) -> np.ndarray:
+    e = getattr(m, "entries", m)
+    return np.asarray(e, dtype=np.float64)
+
+
+def pack(matrices: Sequence) -> dict[str, np.ndarray]:
+    """CSR of every matrix (TransitionMatrix or square ndarray), concatenated.
+
+    Layout (include/cfgsim.h): graph g's row pointer is
+    ``rowptr[rp_off[g] : rp_off[g] + n + 1]`` (local offsets), its entries
+    ``col/val[nz_off[g] : nz_off[g] + nnz_g]`` in row-major order."""
+    k = len(matrices)
+    n_nodes = np.empty(k, np.int32)
+    rp_off = np.empty(k, np.int64)
+    nz_off = np.empty(k, np.int64)
+    rowptrs, cols, vals = [], [], []
+    rp_at = nz_at = 0
+    for g, m in enumerate(matrices):
+        e = _entries(m)
+        if e.ndim != 2 or e.shape[0] != e.shape[1] or e.shape[0] < 1:
+            raise ValueError(f"matrix {g}: entries must be square and non-empty, got {e.shape}")
+        n = e.shape[0]
+        r, c = np.nonzero(e)
+        rp = np.zeros(n + 1, np.int32)
+        np.cumsum(np.bincount(r, minlength=n), out=rp[1:])
+        n_nodes[g] = n
+        rp_off[g] = rp_at
+        nz_off[g] = nz_at
+        rowptrs.append(rp)
+        cols.append(c.astype(np.int32))
+        vals.append(e[r, c])
+        rp_at += n + 1
+        nz_at += len(r)
+    cat = lambda xs, dt: np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0, dt), dt)
+    return dict(n_nodes=n_nodes, rp_off=rp_off, rowptr=cat(rowptrs, np.int32),
+                nz_off=nz_off, col=cat(cols, np.int32), val=cat(vals, np.float64))
+
+
+def packed_bytes(packed: dict) -> int:
+    return int(sum(a.nbytes for a in packed.values()))
+
+
+class DeviceCorpus:
+    """A packed corpus resident in one GPU's HBM (``cfgsim_corpus_create``)."""
+
+    def __init__(self, matrices_or_packed, device: int | None = None):
+        packed = matrices_or_packed if isinstance(matrices_or_packed, dict) else pack(matrices_or_packed)
+        self.device = nat.default_device() if device is None else int(device)
+        self.n_nodes = packed["n_nodes"]
+        self.K = int(len(self.n_nodes))
+        self.h2d_bytes = packed_bytes(packed)
+        h = nat.C.c_void_p()
+        nat.check(nat.lib.cfgsim_corpus_create(
+            self.device, self.K, nat.ptr(packed["n_nodes"]), nat.ptr(packed["rp_off"]),
+            nat.ptr(packed["rowptr"]), nat.ptr(packed["nz_off"]), nat.ptr(packed["col"]),
+            nat.ptr(packed["val"]), nat.C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            nat.lib.cfgsim_corpus_destroy(self._h)
+            self._h = nat.C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- all-pairs over the size-sorted upper triangle (include/cfgsim.h)
+    def n_units(self) -> int:
+        out = np.zeros(1, np.int64)
+        nat.check(nat.lib.cfgsim_allpairs_units(self._h, nat.ptr(out)))
+        return int(out[0])
+
+    def split(self, world: int) -> np.ndarray:
+        b = np.zeros(world + 1, np.int64)
+        nat.check(nat.lib.cfgsim_allpairs_split(self._h, world, nat.ptr(b)))
+        return b

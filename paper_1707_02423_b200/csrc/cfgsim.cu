@@ -1,0 +1,865 @@
+// cfgsim C ABI (include/cfgsim.h): corpus upload, tier scheduling, launches.
+//
+// Replaces the reference's per-pair Python loop (similarity.py:240-246) and
+// measure_distance ISO branch (similarity.py:176-189).  All arithmetic of
+// the pair path runs in isorank.cuh on sm_100a; this file only moves data,
+// buckets pairs into on-chip tiers by N = max(n_a, n_b), and launches
+// persistent kernels that pull pairs from an atomic work counter (pair cost
+// varies ~8x with the data-dependent iteration count).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/cfgsim.h"
+#include "isorank.cuh"
+
+using namespace cfgsim;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? CFGSIM_ERR_NOMEM : CFGSIM_ERR_CUDA, \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// RAII device buffer
+struct DBuf {
+  void *p = nullptr;
+  size_t n = 0;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t bytes) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = bytes;
+    return bytes ? cudaMalloc(&p, bytes) : cudaSuccess;
+  }
+  template <typename T>
+  T *as() const {
+    return (T *)p;
+  }
+};
+
+}  // namespace
+
+struct cfgsim_corpus {
+  int device = 0;
+  int32_t K = 0;
+  int32_t max_nodes = 0;
+  std::vector<int32_t> n_nodes;   // graph order
+  std::vector<int32_t> perm;      // sorted position -> graph (n desc, index asc)
+  std::vector<int32_t> n_sorted;  // n of perm[a]
+  std::vector<int64_t> row_start; // triangle units: K+1
+  DBuf d_n, d_rp_off, d_rowptr, d_nz_off, d_col, d_val, d_perm, d_row_start;
+  int64_t bytes = 0;
+  DevCorpus dev() const {
+    DevCorpus c;
+    c.n_graphs = K;
+    c.n_nodes = d_n.as<int32_t>();
+    c.rp_off = d_rp_off.as<int64_t>();
+    c.rowptr = d_rowptr.as<int32_t>();
+    c.nz_off = d_nz_off.as<int64_t>();
+    c.col = d_col.as<int32_t>();
+    c.val = d_val.as<double>();
+    return c;
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- tiers
+// A tier is one kernel instantiation.  nmax is the largest N it can hold
+// on-chip (lanes cover N+1 columns in phase A).  occ is the CTAs/SM the
+// tier is tuned for (register-limited); the list capacity is whatever
+// shared memory is left at that occupancy, capped by the dense bound.
+struct Tier {
+  int nmax;
+  int kb, nw, r, occ;
+  size_t entry_bytes;
+  const void *fn;
+  size_t (*smem)(int nlim, int cap);
+};
+
+template <typename T, int KB, int NW, int R, int MINB>
+Tier make_tier() {
+  Tier t;
+  t.nmax = 32 * KB - 1;
+  t.kb = KB;
+  t.nw = NW;
+  t.r = R;
+  t.occ = MINB;
+  t.entry_bytes = sizeof(int32_t) + R * sizeof(T);
+  t.fn = (const void *)isorank_pair_kernel<T, KB, NW, R, MINB>;
+  t.smem = [](int nlim, int cap) { return smem_layout<T, R>(nlim, cap).total; };
+  return t;
+}
+
+const std::vector<Tier> &tiers(int precision) {
+  static std::vector<Tier> t64 = {make_tier<double, 1, 4, 4, 5>(), make_tier<double, 2, 8, 4, 2>(),
+                                  make_tier<double, 4, 16, 4, 1>()};
+  static std::vector<Tier> t32 = {make_tier<float, 1, 4, 4, 5>(), make_tier<float, 2, 8, 4, 2>(),
+                                  make_tier<float, 4, 16, 4, 1>()};
+  return precision == CFGSIM_FP32 ? t32 : t64;
+}
+
+constexpr size_t kMaxSmem = 227 * 1024;   // per CTA
+constexpr size_t kSmemPerSM = 228 * 1024; // per SM, incl. 1 KB reserved per CTA
+
+int dense_cap(int nlim, int r) { return ((nlim + r - 1) / r) * nlim; }
+
+// list capacity for a launch of tier T sized for nlim; dense -> dense bound
+int plan_cap(const Tier &T, int nlim, bool dense) {
+  const int dc = dense_cap(nlim, T.r);
+  const size_t base = T.smem(nlim, 0) + 64;
+  if (dense) return (T.smem(nlim, dc) <= kMaxSmem) ? dc : -1;
+  const size_t budget = std::min(kMaxSmem, kSmemPerSM / T.occ - 1024);
+  if (base >= budget) return (T.smem(nlim, std::min(dc, 4 * nlim)) <= kMaxSmem) ? std::min(dc, 4 * nlim) : -1;
+  const int cap = (int)((budget - base) / (2 * T.entry_bytes)) - 8;
+  return std::max(1, std::min(cap, dc));
+}
+
+// smallest tier holding N whose smem fits; -1 if none
+int tier_index(int precision, int N, bool dense, int *cap_out) {
+  const auto &ts = tiers(precision);
+  for (size_t i = 0; i < ts.size(); i++) {
+    if (N > ts[i].nmax) continue;
+    const int cap = plan_cap(ts[i], N, dense);
+    if (cap > 0) {
+      *cap_out = cap;
+      return (int)i;
+    }
+  }
+  return -1;
+}
+
+struct Scratch {
+  DBuf counters, ovf_count, ovf_list;
+  int64_t ovf_cap = 0;
+};
+
+Scratch &scratch_for(int device) {
+  static std::mutex mu;
+  static std::vector<Scratch *> per_dev(64, nullptr);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!per_dev[device]) per_dev[device] = new Scratch();
+  return *per_dev[device];
+}
+
+// Launch one tier over `work` (persistent grid, atomic work counter).
+int launch_tier(int precision, int ti, int nlim, int cap, const DevCorpus &A, const DevCorpus &B,
+                const PairWork &work, const PairOut &out, const cfgsim_params *p,
+                unsigned long long *counter, cudaStream_t st) {
+  const Tier &T = tiers(precision)[ti];
+  const size_t smem = T.smem(nlim, cap);
+  if (smem > kMaxSmem) return fail(CFGSIM_ERR_ARG, "tier shared memory exceeds 227 KB");
+  CU(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev;
+  CU(cudaGetDevice(&dev));
+  int sms = 0, occ = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, T.fn, T.nw * 32, smem));
+  if (occ < 1) return fail(CFGSIM_ERR_CUDA, "tier kernel cannot be resident (occupancy 0)");
+  int64_t grid = (int64_t)sms * occ;
+  if (grid > work.n_items) grid = work.n_items;
+  if (grid < 1) return CFGSIM_OK;
+  PairParams prm;
+  prm.alpha = p->alpha;
+  prm.tol = (precision == CFGSIM_FP32) ? std::max(p->tol, p->tol_fp32) : p->tol;
+  prm.max_iter = p->max_iter;
+  prm.cap = cap;
+  prm.nlim = nlim;
+  CU(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  void *args[] = {(void *)&A, (void *)&B, (void *)&work, (void *)&out, (void *)&prm, (void *)&counter};
+  CU(cudaLaunchKernel(T.fn, dim3((unsigned)grid), dim3(T.nw * 32), args, smem, st));
+  g_launches++;
+  return CFGSIM_OK;
+}
+
+int check_params(const cfgsim_params *p) {
+  if (!p) return fail(CFGSIM_ERR_ARG, "params is NULL");
+  if (!(p->alpha > 0.0 && p->alpha < 1.0))
+    return fail(CFGSIM_ERR_ARG, "alpha must be in (0, 1)");  // similarity.py:129-130
+  if (!(p->tol > 0.0)) return fail(CFGSIM_ERR_ARG, "tol must be positive");
+  if (p->max_iter < 1) return fail(CFGSIM_ERR_ARG, "max_iter must be >= 1");
+  if (p->precision != CFGSIM_FP64 && p->precision != CFGSIM_FP32)
+    return fail(CFGSIM_ERR_ARG, "precision must be CFGSIM_FP64 or CFGSIM_FP32");
+  return CFGSIM_OK;
+}
+
+int set_device(int dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(CFGSIM_ERR_NODEVICE, "no CUDA device: cfgsim has no CPU path");
+  }
+  if (dev < 0 || dev >= n) return fail(CFGSIM_ERR_ARG, "device index out of range");
+  CU(cudaSetDevice(dev));
+  cudaDeviceProp pr;
+  CU(cudaGetDeviceProperties(&pr, dev));
+  if (pr.major != 10) return fail(CFGSIM_ERR_NODEVICE, "cfgsim is built for sm_100a only");
+  return CFGSIM_OK;
+}
+
+// Output staging: device pointers are used in place, host pointers staged.
+struct OutStage {
+  void *user;
+  size_t bytes;
+  DBuf buf;
+  void *dev = nullptr;
+  bool host = false;
+  cudaError_t prepare(void *u, size_t b) {
+    user = u;
+    bytes = b;
+    if (!u) return cudaSuccess;
+    if (is_device_ptr(u)) {
+      dev = u;
+      return cudaSuccess;
+    }
+    host = true;
+    cudaError_t e = buf.alloc(b);
+    dev = buf.p;
+    return e;
+  }
+  cudaError_t finish(cudaStream_t st) {
+    if (user && host) return cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, st);
+    return cudaSuccess;
+  }
+};
+
+// Pair-list execution shared by isorank_pairs / nearest / overflow reruns.
+// ia/ib/slot are host arrays.  Outputs are device arrays indexed by slot.
+int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<int32_t> &ia,
+             const std::vector<int32_t> &ib, const std::vector<int64_t> &slot, const cfgsim_params *p,
+             double *d, double *W, int32_t *iters, uint8_t *conv, double *X, int32_t *match,
+             const double *x0, cudaStream_t st, int cap_mode = 0);
+
+int handle_overflow(const cfgsim_corpus *A, const cfgsim_corpus *B, const PairWork &work,
+                    const cfgsim_params *p, double *d, double *W, int32_t *iters, uint8_t *conv,
+                    Scratch &S, cudaStream_t st) {
+  int32_t cnt = 0;
+  CU(cudaMemcpyAsync(&cnt, S.ovf_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (cnt == 0) return CFGSIM_OK;
+  if (cnt > S.ovf_cap) return fail(CFGSIM_ERR_CUDA, "overflow list capacity exceeded");
+  std::vector<int64_t> recs(cnt);
+  CU(cudaMemcpy(recs.data(), S.ovf_list.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> ia, ib;
+  std::vector<int64_t> sl;
+  for (int64_t rec : recs) {
+    const int64_t item = rec >> 1;
+    const int dir = (int)(rec & 1);
+    if (work.mode == WORK_LIST) {
+      // caller's list arrays are on the device; we kept host copies in work.* (see run_list)
+      return fail(CFGSIM_ERR_CUDA, "internal: list overflow must be handled by run_list");
+    }
+    const int64_t u = work.u0 + item;
+    const auto &rs = A->row_start;
+    const int a = (int)(std::upper_bound(rs.begin(), rs.end(), u) - rs.begin()) - 1;
+    const int b = a + (int)(u - rs[a]);
+    int g1 = A->perm[a], g2 = A->perm[b];
+    if (dir) std::swap(g1, g2);
+    ia.push_back(g1);
+    ib.push_back(g2);
+    sl.push_back(work.ordered ? 2 * (u - work.out_base) + dir : (u - work.out_base));
+  }
+  CU(cudaMemsetAsync(S.ovf_count.p, 0, sizeof(int32_t), st));
+  return run_list(A, B, ia, ib, sl, p, d, W, iters, conv, nullptr, nullptr, nullptr, st, 1);
+}
+
+int ensure_scratch(Scratch &S, int64_t ovf_cap) {
+  if (!S.counters.p) {
+    CU(S.counters.alloc(sizeof(unsigned long long) * 64));
+    CU(S.ovf_count.alloc(sizeof(int32_t)));
+    CU(cudaMemset(S.ovf_count.p, 0, sizeof(int32_t)));
+  }
+  if (S.ovf_cap < ovf_cap) {
+    CU(S.ovf_list.alloc(sizeof(int64_t) * ovf_cap));
+    S.ovf_cap = ovf_cap;
+  }
+  return CFGSIM_OK;
+}
+
+int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<int32_t> &ia,
+             const std::vector<int32_t> &ib, const std::vector<int64_t> &slot, const cfgsim_params *p,
+             double *d, double *W, int32_t *iters, uint8_t *conv, double *X, int32_t *match,
+             const double *x0, cudaStream_t st, int cap_mode) {
+  const int64_t n = (int64_t)ia.size();
+  if (n == 0) return CFGSIM_OK;
+  Scratch &S = scratch_for(A->device);
+  if (int rc = ensure_scratch(S, 1 << 16)) return rc;
+  // bucket by tier, within a tier by descending N (largest first)
+  const int nt = (int)tiers(p->precision).size();
+  std::vector<std::vector<int64_t>> bucket(nt);
+  for (int64_t q = 0; q < n; q++) {
+    const int N = std::max(A->n_nodes[ia[q]], B->n_nodes[ib[q]]);
+    int cap;
+    const int ti = tier_index(p->precision, N, cap_mode != 0, &cap);
+    if (ti < 0)
+      return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
+                                      " exceeds the on-chip tiers of this build");
+    bucket[ti].push_back(q);
+  }
+  for (int ti = 0; ti < nt; ti++) {
+    auto &bk = bucket[ti];
+    if (bk.empty()) continue;
+    std::stable_sort(bk.begin(), bk.end(), [&](int64_t x, int64_t y) {
+      return std::max(A->n_nodes[ia[x]], B->n_nodes[ib[x]]) >
+             std::max(A->n_nodes[ia[y]], B->n_nodes[ib[y]]);
+    });
+    int nlim = 0;
+    std::vector<int32_t> hia(bk.size()), hib(bk.size());
+    std::vector<int64_t> hsl(bk.size());
+    for (size_t q = 0; q < bk.size(); q++) {
+      hia[q] = ia[bk[q]];
+      hib[q] = ib[bk[q]];
+      hsl[q] = slot[bk[q]];
+      nlim = std::max(nlim, std::max(A->n_nodes[hia[q]], B->n_nodes[hib[q]]));
+    }
+    DBuf dia, dib, dsl;
+    CU(dia.alloc(sizeof(int32_t) * bk.size()));
+    CU(dib.alloc(sizeof(int32_t) * bk.size()));
+    CU(dsl.alloc(sizeof(int64_t) * bk.size()));
+    CU(cudaMemcpyAsync(dia.p, hia.data(), sizeof(int32_t) * bk.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dib.p, hib.data(), sizeof(int32_t) * bk.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dsl.p, hsl.data(), sizeof(int64_t) * bk.size(), cudaMemcpyHostToDevice, st));
+    PairWork w{};
+    w.mode = WORK_LIST;
+    w.n_items = (int64_t)bk.size();
+    w.ia = dia.as<int32_t>();
+    w.ib = dib.as<int32_t>();
+    w.slot = dsl.as<int64_t>();
+    PairOut o{};
+    o.d = d;
+    o.W = W;
+    o.iters = iters;
+    o.conv = conv;
+    o.X = X;
+    o.match = match;
+    o.x0 = x0;
+    o.ovf_count = S.ovf_count.as<int32_t>();
+    o.ovf_list = S.ovf_list.as<int64_t>();
+    o.ovf_cap = (int32_t)S.ovf_cap;
+    const int cap2 = plan_cap(tiers(p->precision)[ti], nlim, cap_mode != 0);
+    if (cap2 < 1) return fail(CFGSIM_ERR_ARG, "no list capacity for this tier");
+    if (int rc = launch_tier(p->precision, ti, nlim, cap2, A->dev(), B->dev(), w, o, p,
+                             S.counters.as<unsigned long long>() + ti, st))
+      return rc;
+    // overflowed items: rerun with dense-bound lists
+    int32_t cnt = 0;
+    CU(cudaMemcpyAsync(&cnt, S.ovf_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (cnt > 0) {
+      if (cap_mode) return fail(CFGSIM_ERR_CUDA, "internal: dense-bound lists overflowed");
+      if (cnt > S.ovf_cap) return fail(CFGSIM_ERR_CUDA, "overflow list capacity exceeded");
+      std::vector<int64_t> recs(cnt);
+      CU(cudaMemcpy(recs.data(), S.ovf_list.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+      CU(cudaMemset(S.ovf_count.p, 0, sizeof(int32_t)));
+      std::vector<int32_t> ra, rb;
+      std::vector<int64_t> rs;
+      for (int64_t rec : recs) {
+        const int64_t item = rec >> 1;
+        ra.push_back(hia[item]);
+        rb.push_back(hib[item]);
+        rs.push_back(hsl[item]);
+      }
+      if (int rc = run_list(A, B, ra, rb, rs, p, d, W, iters, conv, X, match, x0, st, 1)) return rc;
+    }
+  }
+  return CFGSIM_OK;
+}
+
+__global__ void scatter_kernel(int64_t n_units, int32_t K, const int64_t *row_start,
+                               const int32_t *perm, int32_t ordered, const double *d_lin,
+                               const int32_t *it_lin, double *d_mat, int32_t *it_mat) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_units;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (row_start[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    const int a = lo, b = a + (int)(u - row_start[a]);
+    const int64_t ga = perm[a], gb = perm[b];
+    const double d0 = ordered ? d_lin[2 * u] : d_lin[u];
+    const double d1 = (ordered && a != b) ? d_lin[2 * u + 1] : d0;
+    d_mat[ga * K + gb] = d0;
+    d_mat[gb * K + ga] = d1;
+    if (it_mat && it_lin) {
+      const int32_t i0 = ordered ? it_lin[2 * u] : it_lin[u];
+      const int32_t i1 = (ordered && a != b) ? it_lin[2 * u + 1] : i0;
+      it_mat[ga * K + gb] = i0;
+      it_mat[gb * K + ga] = i1;
+    }
+  }
+}
+
+// argmin over each row of a (nq x nc) distance block, ties -> lowest column.
+__global__ void rowmin_kernel(int32_t nq, int32_t nc, const double *dmat, int64_t col0,
+                              double *best_d, int64_t *best_i) {
+  const int q = blockIdx.x;
+  if (q >= nq) return;
+  double bv = INFINITY;
+  int64_t bi = INT64_MAX;
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    const double v = dmat[(int64_t)q * nc + c];
+    if (v < bv) { bv = v; bi = c; }  // NaN never wins (np.argmin would; pairs never fail here)
+  }
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  for (int m = 16; m > 0; m >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, m);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, m);
+    if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = bv; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+      if (sv[w] < bv || (sv[w] == bv && si[w] < bi)) { bv = sv[w]; bi = si[w]; }
+    best_d[q] = bv;
+    best_i[q] = (bi == INT64_MAX) ? -1 : bi + col0;
+  }
+}
+
+// interpolate_to on the device (matrix.py:74-106), bit-exact.
+__global__ void interp_kernel(int n, const double *src, int N, double *dst) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * N; e += gridDim.x * blockDim.x) {
+    const int p = e / N, q = e % N;
+    if (n == N) { dst[e] = src[e]; continue; }
+    if (n == 1) { dst[e] = src[0]; continue; }
+    auto lof = [&](int t, int &l, double &f) {
+      const double pos = __ddiv_rn((double)((long long)t * (n - 1)), (double)(N - 1));
+      l = (int)floor(pos);
+      if (l > n - 2) l = n - 2;
+      f = __dsub_rn(pos, (double)l);
+    };
+    int lp, lq;
+    double fp, fq;
+    lof(p, lp, fp);
+    lof(q, lq, fq);
+    const double v00 = src[lp * n + lq], v01 = src[lp * n + lq + 1];
+    const double v10 = src[(lp + 1) * n + lq], v11 = src[(lp + 1) * n + lq + 1];
+    const double omc = __dsub_rn(1.0, fq);
+    const double top = __dadd_rn(__dmul_rn(omc, v00), __dmul_rn(fq, v01));
+    const double bot = __dadd_rn(__dmul_rn(omc, v10), __dmul_rn(fq, v11));
+    dst[e] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, fp), top), __dmul_rn(fp, bot));
+  }
+}
+
+int corpus_from_dense(int device, int n, const double *M, cfgsim_corpus **out) {
+  std::vector<int32_t> rp(n + 1, 0), col;
+  std::vector<double> val;
+  for (int r = 0; r < n; r++) {
+    for (int c = 0; c < n; c++) {
+      const double v = M[(size_t)r * n + c];
+      if (v != 0.0) {
+        col.push_back(c);
+        val.push_back(v);
+      }
+    }
+    rp[r + 1] = (int32_t)col.size();
+  }
+  const int32_t nn = n;
+  const int64_t rpo = 0, nzo = 0;
+  return cfgsim_corpus_create(device, 1, &nn, &rpo, rp.data(), &nzo, col.data(), val.data(), out);
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *cfgsim_last_error(void) { return g_err.c_str(); }
+int cfgsim_version(void) { return 100; }
+int64_t cfgsim_launch_count(void) { return g_launches.load(); }
+
+int cfgsim_device_count(int32_t *n) {
+  if (!n) return fail(CFGSIM_ERR_ARG, "n is NULL");
+  *n = 0;
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return CFGSIM_OK;
+  }
+  for (int i = 0; i < c; i++) {
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, i) == cudaSuccess && pr.major == 10) (*n)++;
+  }
+  return CFGSIM_OK;
+}
+
+int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
+                         const int64_t *rp_off, const int32_t *rowptr, const int64_t *nz_off,
+                         const int32_t *col, const double *val, cfgsim_corpus **out) {
+  if (!out || n_graphs < 1 || !n_nodes || !rp_off || !rowptr || !nz_off)
+    return fail(CFGSIM_ERR_ARG, "bad corpus arguments");
+  if (int rc = set_device(device)) return rc;
+  auto *c = new cfgsim_corpus();
+  c->device = device;
+  c->K = n_graphs;
+  c->n_nodes.assign(n_nodes, n_nodes + n_graphs);
+  int64_t rp_total = 0, nz_total = 0;
+  for (int g = 0; g < n_graphs; g++) {
+    const int n = n_nodes[g];
+    if (n < 1) {
+      delete c;
+      return fail(CFGSIM_ERR_ARG, "graph with no nodes (EmptyGraph)");
+    }
+    c->max_nodes = std::max(c->max_nodes, n);
+    rp_total = std::max(rp_total, rp_off[g] + n + 1);
+    nz_total = std::max(nz_total, nz_off[g] + (int64_t)rowptr[rp_off[g] + n]);
+  }
+  c->perm.resize(n_graphs);
+  std::iota(c->perm.begin(), c->perm.end(), 0);
+  std::stable_sort(c->perm.begin(), c->perm.end(),
+                   [&](int x, int y) { return n_nodes[x] > n_nodes[y]; });
+  c->n_sorted.resize(n_graphs);
+  for (int a = 0; a < n_graphs; a++) c->n_sorted[a] = n_nodes[c->perm[a]];
+  c->row_start.resize(n_graphs + 1);
+  c->row_start[0] = 0;
+  for (int a = 0; a < n_graphs; a++) c->row_start[a + 1] = c->row_start[a] + (n_graphs - a);
+
+  auto up = [&](DBuf &b, const void *src, size_t bytes) -> cudaError_t {
+    cudaError_t e = b.alloc(std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) return e;
+    c->bytes += (int64_t)bytes;
+    return bytes ? cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+  };
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = up(c->d_n, n_nodes, sizeof(int32_t) * n_graphs);
+  if (e == cudaSuccess) e = up(c->d_rp_off, rp_off, sizeof(int64_t) * n_graphs);
+  if (e == cudaSuccess) e = up(c->d_rowptr, rowptr, sizeof(int32_t) * rp_total);
+  if (e == cudaSuccess) e = up(c->d_nz_off, nz_off, sizeof(int64_t) * n_graphs);
+  if (e == cudaSuccess) e = up(c->d_col, col, sizeof(int32_t) * nz_total);
+  if (e == cudaSuccess) e = up(c->d_val, val, sizeof(double) * nz_total);
+  if (e == cudaSuccess) e = up(c->d_perm, c->perm.data(), sizeof(int32_t) * n_graphs);
+  if (e == cudaSuccess) e = up(c->d_row_start, c->row_start.data(), sizeof(int64_t) * (n_graphs + 1));
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(e == cudaErrorMemoryAllocation ? CFGSIM_ERR_NOMEM : CFGSIM_ERR_CUDA,
+                std::string("corpus upload: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return CFGSIM_OK;
+}
+
+int cfgsim_corpus_destroy(cfgsim_corpus *c) {
+  if (c) {
+    cudaSetDevice(c->device);
+    delete c;
+  }
+  return CFGSIM_OK;
+}
+
+int cfgsim_corpus_info(const cfgsim_corpus *c, int32_t *n_graphs, int32_t *max_nodes,
+                       int64_t *device_bytes) {
+  if (!c) return fail(CFGSIM_ERR_ARG, "corpus is NULL");
+  if (n_graphs) *n_graphs = c->K;
+  if (max_nodes) *max_nodes = c->max_nodes;
+  if (device_bytes) *device_bytes = c->bytes;
+  return CFGSIM_OK;
+}
+
+int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_pairs,
+                         const int32_t *ia, const int32_t *ib, const cfgsim_params *p, double *d,
+                         double *W, int32_t *iters, uint8_t *converged, void *cuda_stream) {
+  if (!A || !B || n_pairs < 0 || (n_pairs && (!ia || !ib)))
+    return fail(CFGSIM_ERR_ARG, "bad pair arguments");
+  if (int rc = check_params(p)) return rc;
+  if (A->device != B->device) return fail(CFGSIM_ERR_ARG, "corpora live on different devices");
+  if (int rc = set_device(A->device)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  std::vector<int32_t> ha(n_pairs), hb(n_pairs);
+  if (n_pairs) {
+    CU(cudaMemcpyAsync(ha.data(), ia, sizeof(int32_t) * n_pairs, cudaMemcpyDefault, st));
+    CU(cudaMemcpyAsync(hb.data(), ib, sizeof(int32_t) * n_pairs, cudaMemcpyDefault, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  for (int64_t q = 0; q < n_pairs; q++)
+    if (ha[q] < 0 || ha[q] >= A->K || hb[q] < 0 || hb[q] >= B->K)
+      return fail(CFGSIM_ERR_ARG, "pair index out of range");
+  std::vector<int64_t> slot(n_pairs);
+  std::iota(slot.begin(), slot.end(), 0);
+  OutStage sd, sw, si, sc;
+  CU(sd.prepare(d, sizeof(double) * n_pairs));
+  CU(sw.prepare(W, sizeof(double) * n_pairs));
+  CU(si.prepare(iters, sizeof(int32_t) * n_pairs));
+  CU(sc.prepare(converged, sizeof(uint8_t) * n_pairs));
+  if (int rc = run_list(A, B, ha, hb, slot, p, (double *)sd.dev, (double *)sw.dev,
+                        (int32_t *)si.dev, (uint8_t *)sc.dev, nullptr, nullptr, nullptr, st))
+    return rc;
+  CU(cudaGetLastError());
+  CU(sd.finish(st));
+  CU(sw.finish(st));
+  CU(si.finish(st));
+  CU(sc.finish(st));
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+int cfgsim_allpairs_units(const cfgsim_corpus *c, int64_t *n_units) {
+  if (!c || !n_units) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  *n_units = c->row_start[c->K];
+  return CFGSIM_OK;
+}
+
+int cfgsim_allpairs_split(const cfgsim_corpus *c, int32_t world, int64_t *bounds) {
+  if (!c || world < 1 || !bounds) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  // cost of unit (a, b>=a) ~ N^2 with N = n_sorted[a] (rows sorted by n desc)
+  std::vector<double> cum(c->K + 1, 0.0);
+  for (int a = 0; a < c->K; a++)
+    cum[a + 1] = cum[a] + (double)(c->K - a) * (double)c->n_sorted[a] * c->n_sorted[a];
+  const double total = cum[c->K];
+  bounds[0] = 0;
+  for (int r = 1; r < world; r++) {
+    const double target = total * r / world;
+    const int a = (int)(std::upper_bound(cum.begin(), cum.end(), target) - cum.begin()) - 1;
+    const double per = (double)c->n_sorted[std::min(a, c->K - 1)] * c->n_sorted[std::min(a, c->K - 1)];
+    int64_t u = c->row_start[a] + (int64_t)std::ceil((target - cum[a]) / per);
+    u = std::min<int64_t>(u, c->row_start[std::min(a + 1, c->K)]);
+    bounds[r] = std::max(u, bounds[r - 1]);
+  }
+  bounds[world] = c->row_start[c->K];
+  return CFGSIM_OK;
+}
+
+int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_t ordered,
+                          const cfgsim_params *p, double *d_lin, int32_t *iters_lin,
+                          void *cuda_stream) {
+  if (!c || u0 < 0 || u1 < u0 || u1 > c->row_start[c->K])
+    return fail(CFGSIM_ERR_ARG, "bad unit range");
+  if (int rc = check_params(p)) return rc;
+  if (int rc = set_device(c->device)) return rc;
+  if (u1 == u0) return CFGSIM_OK;
+  if ((d_lin && !is_device_ptr(d_lin)) || (iters_lin && !is_device_ptr(iters_lin)))
+    return fail(CFGSIM_ERR_ARG, "allpairs_range outputs must be device pointers");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  Scratch &S = scratch_for(c->device);
+  if (int rc = ensure_scratch(S, 1 << 16)) return rc;
+  const int nt = (int)tiers(p->precision).size();
+  // rows of the sorted corpus with N in a tier are contiguous: split the unit
+  // range at tier boundaries (n_sorted is descending).
+  int a = (int)(std::upper_bound(c->row_start.begin(), c->row_start.end(), u0) -
+                c->row_start.begin()) - 1;
+  int64_t u = u0;
+  int launch_no = 0;
+  while (u < u1) {
+    const int N = c->n_sorted[a];
+    int cap;
+    const int ti = tier_index(p->precision, N, false, &cap);
+    if (ti < 0)
+      return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
+                                      " exceeds the on-chip tiers of this build");
+    // extend over rows in the same tier
+    int a_end = a;
+    int cap_e;
+    while (a_end + 1 < c->K && tier_index(p->precision, c->n_sorted[a_end + 1], false, &cap_e) == ti)
+      a_end++;
+    const int64_t seg_end = std::min(u1, c->row_start[a_end + 1]);
+    PairWork w{};
+    w.mode = WORK_TRIANGLE;
+    w.ordered = ordered;
+    w.n_items = seg_end - u;
+    w.u0 = u;
+    w.out_base = u0;
+    w.row_start = c->d_row_start.as<int64_t>();
+    w.perm = c->d_perm.as<int32_t>();
+    w.K = c->K;
+    PairOut o{};
+    o.d = d_lin;
+    o.iters = iters_lin;
+    o.ovf_count = S.ovf_count.as<int32_t>();
+    o.ovf_list = S.ovf_list.as<int64_t>();
+    o.ovf_cap = (int32_t)S.ovf_cap;
+    if (launch_no >= 60) return fail(CFGSIM_ERR_CUDA, "too many tier segments");
+    if (int rc = launch_tier(p->precision, ti, N, cap, c->dev(), c->dev(), w, o, p,
+                             S.counters.as<unsigned long long>() + launch_no, st))
+      return rc;
+    launch_no++;
+    if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
+    u = seg_end;
+    a = a_end + 1;
+    (void)nt;
+  }
+  CU(cudaGetLastError());
+  return CFGSIM_OK;
+}
+
+int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const double *d_lin,
+                            const int32_t *iters_lin, double *d_mat, int32_t *iters_mat,
+                            void *cuda_stream) {
+  if (!c || !d_lin || !d_mat) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  if (int rc = set_device(c->device)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t nu = c->row_start[c->K];
+  g_launches++;
+  scatter_kernel<<<1184, 256, 0, st>>>(nu, c->K, c->d_row_start.as<int64_t>(),
+                                       c->d_perm.as<int32_t>(), ordered, d_lin, iters_lin, d_mat,
+                                       iters_mat);
+  CU(cudaGetLastError());
+  return CFGSIM_OK;
+}
+
+int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params *p,
+                    double *d_mat, int32_t *iters_mat, void *cuda_stream) {
+  if (!c || !d_mat) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  if (int rc = check_params(p)) return rc;
+  if (int rc = set_device(c->device)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t nu = c->row_start[c->K];
+  const int64_t slots = ordered ? 2 * nu : nu;
+  DBuf dl, il;
+  CU(dl.alloc(sizeof(double) * slots));
+  if (iters_mat) CU(il.alloc(sizeof(int32_t) * slots));
+  if (int rc = cfgsim_allpairs_range(c, 0, nu, ordered, p, dl.as<double>(), il.as<int32_t>(), st))
+    return rc;
+  const size_t KK = (size_t)c->K * c->K;
+  OutStage sd, si;
+  CU(sd.prepare(d_mat, sizeof(double) * KK));
+  CU(si.prepare(iters_mat, sizeof(int32_t) * KK));
+  if (int rc = cfgsim_allpairs_scatter(c, ordered, dl.as<double>(), il.as<int32_t>(),
+                                       (double *)sd.dev, (int32_t *)si.dev, st))
+    return rc;
+  CU(sd.finish(st));
+  CU(si.finish(st));
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+int cfgsim_isorank_single(int32_t device, int32_t na, const double *A, int32_t nb,
+                          const double *B, const cfgsim_params *p, const double *x0,
+                          double *X_out, int32_t *match_out, double *d, double *W,
+                          int32_t *iters, uint8_t *converged) {
+  if (na < 1 || nb < 1 || !A || !B) return fail(CFGSIM_ERR_ARG, "bad matrices");
+  if (int rc = check_params(p)) return rc;
+  if (int rc = set_device(device)) return rc;
+  cfgsim_corpus *ca = nullptr, *cb = nullptr;
+  if (int rc = corpus_from_dense(device, na, A, &ca)) return rc;
+  if (int rc = corpus_from_dense(device, nb, B, &cb)) {
+    cfgsim_corpus_destroy(ca);
+    return rc;
+  }
+  const int N = std::max(na, nb);
+  DBuf dd, dw, di, dc, dX, dm, dx0;
+  int rc = CFGSIM_OK;
+  auto cu = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == CFGSIM_OK)
+      rc = fail(CFGSIM_ERR_CUDA, std::string("single: ") + cudaGetErrorString(e));
+    return e == cudaSuccess;
+  };
+  cu(dd.alloc(8));
+  cu(dw.alloc(8));
+  cu(di.alloc(4));
+  cu(dc.alloc(1));
+  cu(dX.alloc(sizeof(double) * N * N));
+  cu(dm.alloc(sizeof(int32_t) * N));
+  if (x0) {
+    cu(dx0.alloc(sizeof(double) * N * N));
+    cu(cudaMemcpy(dx0.p, x0, sizeof(double) * N * N, cudaMemcpyHostToDevice));
+  }
+  if (rc == CFGSIM_OK) {
+    std::vector<int32_t> ia{0}, ib{0};
+    std::vector<int64_t> sl{0};
+    rc = run_list(ca, cb, ia, ib, sl, p, dd.as<double>(), dw.as<double>(), di.as<int32_t>(),
+                  dc.as<uint8_t>(), dX.as<double>(), dm.as<int32_t>(), dx0.as<double>(), 0);
+  }
+  if (rc == CFGSIM_OK) cu(cudaDeviceSynchronize());
+  if (rc == CFGSIM_OK) {
+    if (d) cu(cudaMemcpy(d, dd.p, 8, cudaMemcpyDeviceToHost));
+    if (W) cu(cudaMemcpy(W, dw.p, 8, cudaMemcpyDeviceToHost));
+    if (iters) cu(cudaMemcpy(iters, di.p, 4, cudaMemcpyDeviceToHost));
+    if (converged) cu(cudaMemcpy(converged, dc.p, 1, cudaMemcpyDeviceToHost));
+    if (X_out) cu(cudaMemcpy(X_out, dX.p, sizeof(double) * N * N, cudaMemcpyDeviceToHost));
+    if (match_out) cu(cudaMemcpy(match_out, dm.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost));
+  }
+  cfgsim_corpus_destroy(ca);
+  cfgsim_corpus_destroy(cb);
+  return rc;
+}
+
+int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, int32_t c1,
+                   const cfgsim_params *p, double *best_d, int64_t *best_idx, void *cuda_stream) {
+  if (!Q || !C || c0 < 0 || c1 > C->K || c1 <= c0 || !best_d || !best_idx)
+    return fail(CFGSIM_ERR_ARG, "bad nearest arguments");
+  if (int rc = check_params(p)) return rc;
+  if (Q->device != C->device) return fail(CFGSIM_ERR_ARG, "corpora live on different devices");
+  if (int rc = set_device(Q->device)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int32_t nq = Q->K, nc = c1 - c0;
+  OutStage sd, si;
+  CU(sd.prepare(best_d, sizeof(double) * nq));
+  CU(si.prepare(best_idx, sizeof(int64_t) * nq));
+  // query blocks so that one block's distance matrix stays <= ~2^27 entries
+  const int64_t per_block = std::max<int64_t>(1, ((int64_t)1 << 27) / nc);
+  DBuf dm;
+  CU(dm.alloc(sizeof(double) * std::min<int64_t>(nq, per_block) * nc));
+  for (int32_t q0 = 0; q0 < nq; q0 += (int32_t)per_block) {
+    const int32_t q1 = (int32_t)std::min<int64_t>(nq, q0 + per_block);
+    std::vector<int32_t> ia, ib;
+    std::vector<int64_t> sl;
+    ia.reserve((size_t)(q1 - q0) * nc);
+    ib.reserve((size_t)(q1 - q0) * nc);
+    sl.reserve((size_t)(q1 - q0) * nc);
+    for (int32_t q = q0; q < q1; q++)
+      for (int32_t j = 0; j < nc; j++) {
+        ia.push_back(q);
+        ib.push_back(c0 + j);
+        sl.push_back((int64_t)(q - q0) * nc + j);
+      }
+    if (int rc = run_list(Q, C, ia, ib, sl, p, dm.as<double>(), nullptr, nullptr, nullptr, nullptr,
+                          nullptr, nullptr, st))
+      return rc;
+    rowmin_kernel<<<q1 - q0, 256, 0, st>>>(q1 - q0, nc, dm.as<double>(), c0,
+                                           (double *)sd.dev + q0, (int64_t *)si.dev + q0);
+    CU(cudaGetLastError());
+  }
+  CU(sd.finish(st));
+  CU(si.finish(st));
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+int cfgsim_interpolate(int32_t device, int32_t n, const double *src, int32_t target, double *dst) {
+  if (n < 1 || target < n || !src || !dst) return fail(CFGSIM_ERR_ARG, "bad interpolation arguments");
+  if (int rc = set_device(device)) return rc;
+  DBuf s, d;
+  CU(s.alloc(sizeof(double) * n * n));
+  CU(d.alloc(sizeof(double) * target * target));
+  CU(cudaMemcpy(s.p, src, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  interp_kernel<<<(target * target + 255) / 256, 256>>>(n, s.as<double>(), target, d.as<double>());
+  CU(cudaGetLastError());
+  CU(cudaMemcpy(dst, d.p, sizeof(double) * target * target, cudaMemcpyDeviceToHost));
+  return CFGSIM_OK;
+}
+
+}  // extern "C"

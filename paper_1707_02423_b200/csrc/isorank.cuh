@@ -1,0 +1,754 @@
+// IsoRank pair kernel for sm_100a — one CTA per CFG pair, state on-chip.
+//
+// Computes, per pair (a, b), exactly the reference's ISO measure
+//   measure_distance(a, b, ISO)       similarity.py:176-189
+//   = isorank_distance(isorank_align(normalize_pair(a, b)))
+// with the Kronecker mat-vec kron(A',B')^T x (similarity.py:133,140)
+// evaluated as the two sparse products  Y = A'^T X,  Z = Y B'.
+//
+// Layout (shared memory, per CTA):
+//   Xs  (N+1) x P   X state (unnormalised F of the last sweep, scale r_old)
+//                   + padding column N (g = X z_B) and row N (unused)
+//   Ys  (N+1) x P   Y = A'^T X (+ column N: v = Y z_B)
+//   lists A, B      column-tile lists of the row-normalised operators:
+//                   tile t covers R consecutive columns; entry = (row i,
+//                   R weights).  Uniform (zero-sum) rows are excluded and
+//                   applied as rank-1 terms (u = z_A^T X, v = Y z_B).
+//   P = (N+1)|1 (odd) so that column accesses with lanes over rows are
+//   bank-conflict free for 8-byte elements.
+// Each sweep (3 CTA barriers):
+//   U: u[j] = sum_{i in zA} X[i,j];  X[i,N] = sum_{j in zB} X[i,j]
+//   A: lanes over columns j (0..N), warps over row tiles of Y:
+//        Y[k,j] = sum_e w_e[k] X[i_e,j] + u[j]/N       (column N gives v)
+//   B: lanes over rows k, warps over column tiles of Z:
+//        F[k,l] = (alpha*r_old) (sum_e w_e[l] Y[k,j_e] + v[k]/N) + (1-alpha)/N^2
+//      reduce s = sum F, dp = sum |F - X_old|, m = sum sign(F - X_old) F
+//   delta = sum |F/s - X_old| = dp + (1/s - 1) m   (exact to first order in
+//   |1-s| ~ 1e-16), stop when delta < tol
+//   (similarity.py:141-146).  X_old lives in registers of its owner thread.
+// Epilogue: greedy matching with cached row maxima (same tie rule as
+// similarity.py:96-108), W, d (similarity.py:150,160-173).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cfgsim {
+
+struct DevCorpus {
+  int32_t n_graphs;
+  const int32_t *n_nodes;
+  const int64_t *rp_off;
+  const int32_t *rowptr;
+  const int64_t *nz_off;
+  const int32_t *col;
+  const double *val;
+};
+
+enum { WORK_LIST = 0, WORK_TRIANGLE = 1 };
+
+struct PairWork {
+  int32_t mode;
+  int32_t ordered;   // triangle: compute both directions separately
+  int64_t n_items;   // items in this launch
+  // list mode
+  const int32_t *ia;
+  const int32_t *ib;
+  const int64_t *slot;  // output slot per item (NULL: slot = item)
+  // triangle mode: unit u = u0 + item; rows of the size-sorted corpus
+  int64_t u0;
+  int64_t out_base;          // unit that maps to output slot 0
+  const int64_t *row_start;  // K+1
+  const int32_t *perm;       // sorted position -> graph index
+  int32_t K;
+};
+
+struct PairOut {
+  double *d;
+  double *W;
+  int32_t *iters;
+  uint8_t *conv;
+  double *X;          // single-pair: N*N normalised alignment matrix
+  int32_t *match;     // single-pair: N
+  const double *x0;   // single-pair: start / sum(start)
+  int32_t *ovf_count; // overflowed (item, dir) records
+  int64_t *ovf_list;
+  int32_t ovf_cap;
+};
+
+struct PairParams {
+  double alpha;
+  double tol;
+  int32_t max_iter;
+  int32_t cap;   // list entries per side
+  int32_t nlim;  // max N this launch is sized for
+};
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ double shfl_xor_d(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+// numpy DOUBLE_pairwise_sum order (umath/loops_utils.h.src), stride 1 —
+// the order of `out.sum(axis=1)` in similarity.py:89.  One thread.
+__device__ double np_pairwise_leaf(const double *a, int n) {  // n <= 128
+  if (n < 8) {
+    double res = 0.;
+    for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) r[k] = a[k];
+  int i;
+  for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], a[i + k]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// The recursion `pw(a, n2) + pw(a + n2, n - n2)` (n2 = n/2 rounded down to a
+// multiple of 8) unrolled with an explicit stack.
+__device__ double np_pairwise_sum(const double *a, int n) {
+  if (n <= 128) return np_pairwise_leaf(a, n);
+  int off[24], len[24], state[24];
+  double left[24];
+  int sp = 0;
+  off[0] = 0; len[0] = n; state[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    if (len[sp] <= 128) {
+      ret = np_pairwise_leaf(a + off[sp], len[sp]);
+      sp--;
+      continue;
+    }
+    int n2 = len[sp] / 2;
+    n2 -= n2 % 8;
+    if (state[sp] == 0) {
+      state[sp] = 1;
+      off[sp + 1] = off[sp]; len[sp + 1] = n2; state[sp + 1] = 0;
+      sp++;
+    } else if (state[sp] == 1) {
+      left[sp] = ret;
+      state[sp] = 2;
+      off[sp + 1] = off[sp] + n2; len[sp + 1] = len[sp] - n2; state[sp + 1] = 0;
+      sp++;
+    } else {
+      ret = __dadd_rn(left[sp], ret);
+      sp--;
+    }
+  }
+  return ret;
+}
+
+// R consecutive weights as one or two 16-byte shared loads (broadcast).
+template <typename T, int R>
+__device__ __forceinline__ void load_w(const T *p, T (&w)[R]) {
+  if constexpr (sizeof(T) == 8 && R % 2 == 0) {
+#pragma unroll
+    for (int r = 0; r < R; r += 2) {
+      const double2 v = *reinterpret_cast<const double2 *>(p + r);
+      w[r] = v.x;
+      w[r + 1] = v.y;
+    }
+  } else if constexpr (sizeof(T) == 4 && R % 4 == 0) {
+#pragma unroll
+    for (int r = 0; r < R; r += 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(p + r);
+      w[r] = v.x; w[r + 1] = v.y; w[r + 2] = v.z; w[r + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; r++) w[r] = p[r];
+  }
+}
+
+// warp argmax with key (value desc, index asc) — the first-occurrence rule of
+// np.argmax over a row-major scan.
+template <typename T>
+__device__ __forceinline__ void warp_argmax(T &v, int &idx) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    T ov = __shfl_xor_sync(0xffffffffu, v, m);
+    int oi = __shfl_xor_sync(0xffffffffu, idx, m);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+}
+
+// Shared-memory carve-up, identical on host and device.
+struct Smem {
+  size_t x, y, idxA, wA, idxB, wB, toffA, toffB, zA, zB, uS, lo, fr, zflag, red, misc, total;
+};
+
+template <typename T, int R>
+__host__ __device__ inline Smem smem_layout(int nlim, int cap) {
+  Smem s;
+  const int pm = (nlim + 1) | 1;
+  const int ktm = (nlim + R - 1) / R;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += (bytes + 15) & ~size_t(15);
+    return at;
+  };
+  const size_t xbytes = sizeof(T) * ((size_t)(nlim + 1) * pm + 64);
+  s.x = take(xbytes);
+  s.y = take(xbytes);
+  s.idxA = take(sizeof(int32_t) * (size_t)cap);
+  s.wA = take(sizeof(T) * (size_t)cap * R);
+  s.idxB = take(sizeof(int32_t) * (size_t)cap);
+  s.wB = take(sizeof(T) * (size_t)cap * R);
+  s.toffA = take(sizeof(int32_t) * (ktm + 1));
+  s.toffB = take(sizeof(int32_t) * (ktm + 1));
+  s.zA = take(sizeof(int32_t) * (nlim + 1));
+  s.zB = take(sizeof(int32_t) * (nlim + 1));
+  s.uS = take(sizeof(T) * (nlim + 64));
+  s.lo = take(sizeof(int32_t) * (nlim + 1));
+  s.fr = take(sizeof(double) * (nlim + 1));
+  s.zflag = take(sizeof(uint8_t) * (nlim + 1));
+  s.red = take(sizeof(double) * 3 * 32);
+  s.misc = take(64);
+  s.total = o;
+  return s;
+}
+
+// Build the row-normalised operator of one side (similarity.py:85-93 after
+// matrix.py:74-106) into the dense fp64 scratch `dense` (N x N, pitch N),
+// then extract its column-tile lists.  Returns false on list overflow.
+template <typename T, int KB, int NW, int R>
+__device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dense, int32_t *lo_s,
+                           double *fr_s, uint8_t *zflag, int32_t *zlist, int32_t *nz_out,
+                           int32_t *toff, int32_t *idx, T *wts, int cap, bool premul_rows,
+                           int32_t *misc) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = NW * 32;
+  const int n = G.n_nodes[g];
+  const int32_t *rp = G.rowptr + G.rp_off[g];
+  const int32_t *cc = G.col + G.nz_off[g];
+  const double *vv = G.val + G.nz_off[g];
+  const bool interp = (n != N) && (n > 1);
+
+  if (interp) {  // matrix.py:93-95
+    for (int p = tid; p < N; p += NT) {
+      double pos = __ddiv_rn((double)((long long)p * (n - 1)), (double)(N - 1));
+      int l = (int)floor(pos);
+      if (l > n - 2) l = n - 2;
+      lo_s[p] = l;
+      fr_s[p] = __dsub_rn(pos, (double)l);
+    }
+    __syncthreads();
+  }
+
+  // Rows of A-hat, one warp per target row.
+  for (int p = warp; p < N; p += NW) {
+    double *row = dense + (size_t)p * N;
+    if (n == N) {
+      for (int q = lane; q < N; q += 32) row[q] = 0.0;
+      __syncwarp();
+      for (int e = rp[p] + lane; e < rp[p + 1]; e += 32) row[cc[e]] = vv[e];
+    } else if (n == 1) {  // matrix.py:87-89
+      const double c = (rp[1] > rp[0]) ? vv[0] : 0.0;
+      for (int q = lane; q < N; q += 32) row[q] = c;
+    } else {  // matrix.py:97-104, same operation order, no contraction
+      const int r0 = lo_s[p];
+      const double frp = fr_s[p];
+      const int b0 = rp[r0], e0 = rp[r0 + 1], e1 = rp[r0 + 2];
+      for (int q = lane; q < N; q += 32) {
+        const int c = lo_s[q];
+        const double fc = fr_s[q];
+        double v00 = 0, v01 = 0, v10 = 0, v11 = 0;
+        for (int e = b0; e < e0; e++) {
+          const int k = cc[e];
+          if (k == c) v00 = vv[e];
+          if (k == c + 1) v01 = vv[e];
+        }
+        for (int e = e0; e < e1; e++) {
+          const int k = cc[e];
+          if (k == c) v10 = vv[e];
+          if (k == c + 1) v11 = vv[e];
+        }
+        const double omc = __dsub_rn(1.0, fc);
+        const double top = __dadd_rn(__dmul_rn(omc, v00), __dmul_rn(fc, v01));
+        const double bot = __dadd_rn(__dmul_rn(omc, v10), __dmul_rn(fc, v11));
+        row[q] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, frp), top), __dmul_rn(frp, bot));
+      }
+    }
+    __syncwarp();
+    double s = 0.0;
+    if (lane == 0) s = np_pairwise_sum(row, N);  // similarity.py:89
+    s = shfl_d(s, 0);
+    if (lane == 0) zflag[p] = (s == 0.0);
+    if (s != 0.0)
+      for (int q = lane; q < N; q += 32) row[q] = __ddiv_rn(row[q], s);  // :92
+  }
+  __syncthreads();
+
+  // zero-row list (ascending) and column-tile entry counts
+  const int KT = (N + R - 1) / R;
+  if (warp == 0) {
+    int cnt = 0;
+#pragma unroll
+    for (int c = 0; c < KB; c++) {
+      const int i = lane + 32 * c;
+      const bool z = (i < N) && zflag[i];
+      const unsigned bal = __ballot_sync(0xffffffffu, z);
+      if (z) zlist[cnt + __popc(bal & ((1u << lane) - 1))] = i;
+      cnt += __popc(bal);
+    }
+    if (lane == 0) *nz_out = cnt;
+  }
+  for (int t = warp; t < KT; t += NW) {
+    int cnt = 0;
+#pragma unroll
+    for (int c = 0; c < KB; c++) {
+      const int i = lane + 32 * c;
+      bool nzr = false;
+      if (i < N && !zflag[i]) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const int k = t * R + r;
+          if (k < N && dense[(size_t)i * N + k] != 0.0) nzr = true;
+        }
+      }
+      cnt += __popc(__ballot_sync(0xffffffffu, nzr));
+    }
+    if (lane == 0) toff[t + 1] = cnt;
+  }
+  __syncthreads();
+  if (warp == 0) {  // inclusive scan of tile counts (KT <= 32 * KB / R * ... small)
+    int carry = 0;
+    for (int base = 0; base < KT; base += 32) {
+      const int t = base + lane;
+      int v = (t < KT) ? toff[t + 1] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (t < KT) toff[t + 1] = v + carry;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) {
+      toff[0] = 0;
+      misc[0] = (carry > cap) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (misc[0]) return false;
+  for (int t = warp; t < KT; t += NW) {
+    int pos = toff[t];
+#pragma unroll
+    for (int c = 0; c < KB; c++) {
+      const int i = lane + 32 * c;
+      bool nzr = false;
+      double w[R];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int k = t * R + r;
+        w[r] = (i < N && k < N) ? dense[(size_t)i * N + k] : 0.0;
+        if (w[r] != 0.0) nzr = true;
+      }
+      if (i >= N || zflag[i]) nzr = false;
+      const unsigned bal = __ballot_sync(0xffffffffu, nzr);
+      if (nzr) {
+        const int e = pos + __popc(bal & ((1u << lane) - 1));
+        idx[e] = premul_rows ? i * P : i;
+#pragma unroll
+        for (int r = 0; r < R; r++) wts[(size_t)e * R + r] = (T)w[r];
+      }
+      pos += __popc(bal);
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+template <typename T, int KB, int NW, int R, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    isorank_pair_kernel(DevCorpus CA, DevCorpus CB, PairWork work, PairOut out, PairParams prm,
+                        unsigned long long *counter) {
+  constexpr int NT = NW * 32;
+  constexpr int MAXT = ((32 * KB + R - 1) / R + NW - 1) / NW;  // column tiles per warp (phase B)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Smem L = smem_layout<T, R>(prm.nlim, prm.cap);
+  T *Xs = (T *)(smem_raw + L.x);
+  T *Ys = (T *)(smem_raw + L.y);
+  double *dense = (double *)(smem_raw + L.x);  // prologue scratch (spans Xs, Ys)
+  int32_t *idxA = (int32_t *)(smem_raw + L.idxA);
+  T *wA = (T *)(smem_raw + L.wA);
+  int32_t *idxB = (int32_t *)(smem_raw + L.idxB);
+  T *wB = (T *)(smem_raw + L.wB);
+  int32_t *toffA = (int32_t *)(smem_raw + L.toffA);
+  int32_t *toffB = (int32_t *)(smem_raw + L.toffB);
+  int32_t *zA = (int32_t *)(smem_raw + L.zA);
+  int32_t *zB = (int32_t *)(smem_raw + L.zB);
+  T *uS = (T *)(smem_raw + L.uS);
+  int32_t *lo_s = (int32_t *)(smem_raw + L.lo);
+  double *fr_s = (double *)(smem_raw + L.fr);
+  uint8_t *zflag = (uint8_t *)(smem_raw + L.zflag);
+  double *red = (double *)(smem_raw + L.red);
+  int32_t *misc = (int32_t *)(smem_raw + L.misc);
+  int64_t *s_item = (int64_t *)(misc + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (;;) {
+    if (tid == 0) *s_item = (int64_t)atomicAdd(counter, 1ull);
+    __syncthreads();
+    const int64_t item = *s_item;
+    if (item >= work.n_items) break;
+
+    // ---- decode the work item
+    int ga, gb, ndir = 1;
+    int64_t slot0;
+    if (work.mode == WORK_LIST) {
+      ga = work.ia[item];
+      gb = work.ib[item];
+      slot0 = work.slot ? work.slot[item] : item;
+    } else {
+      const int64_t u = work.u0 + item;
+      int lo = 0, hi = work.K - 1;  // largest a with row_start[a] <= u
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (work.row_start[mid] <= u) lo = mid; else hi = mid - 1;
+      }
+      const int a = lo;
+      const int b = a + (int)(u - work.row_start[a]);
+      ga = work.perm[a];
+      gb = work.perm[b];
+      if (work.ordered) {
+        slot0 = 2 * (u - work.out_base);
+        ndir = (a == b) ? 1 : 2;
+      } else {
+        slot0 = u - work.out_base;
+      }
+    }
+
+    for (int dir = 0; dir < ndir; dir++) {
+      const int g1 = dir ? gb : ga, g2 = dir ? ga : gb;
+      const int64_t slot = slot0 + dir;
+      const int na = CA.n_nodes[g1];
+      const int nb = (dir ? CA : CB).n_nodes[g2];
+      // dir == 1 only occurs in triangle mode, where CA and CB are the same corpus
+      const DevCorpus &C2 = dir ? CA : CB;
+      const int N = na > nb ? na : nb;
+      const int P = (N + 1) | 1;
+      const int KT = (N + R - 1) / R;
+      const double invN = 1.0 / (double)N;
+
+      // ---- prologue: both operators (normalize_pair + _row_normalized)
+      int32_t *nzA = misc + 1, *nzB = misc + 2;
+      bool ok = build_side<T, KB, NW, R>(dir ? CB : CA, g1, N, P, dense, lo_s, fr_s, zflag, zA, nzA,
+                                         toffA, idxA, wA, prm.cap, true, misc);
+      if (ok)
+        ok = build_side<T, KB, NW, R>(C2, g2, N, P, dense, lo_s, fr_s, zflag, zB, nzB, toffB, idxB,
+                                      wB, prm.cap, false, misc);
+      if (!ok) {
+        if (tid == 0) {
+          const int k = atomicAdd(out.ovf_count, 1);
+          if (k < out.ovf_cap) out.ovf_list[k] = item * 2 + dir;
+          if (out.iters) out.iters[slot] = -1;
+        }
+        __syncthreads();
+        continue;
+      }
+      const int nzAv = *nzA, nzBv = *nzB;
+
+      // ---- X_0 (similarity.py:134-135)
+      const double uni = 1.0 / (double)((long long)N * N);
+      for (int e = tid; e < (N + 1) * P; e += NT) {
+        const int i = e / P, j = e - (e / P) * P;
+        T v = 0;
+        if (i < N && j < N) v = out.x0 ? (T)out.x0[(size_t)i * N + j] : (T)uni;
+        Xs[e] = v;
+      }
+      // owned elements (phase B mapping): rows k = lane + 32c, cols l = t*R + r
+      T xold[MAXT][KB][R];
+#pragma unroll
+      for (int m = 0; m < MAXT; m++)
+#pragma unroll
+        for (int c = 0; c < KB; c++)
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            const int k = lane + 32 * c, l = (warp + m * NW) * R + r;
+            xold[m][c][r] = (k < N && l < N) ? (out.x0 ? (T)out.x0[(size_t)k * N + l] : (T)uni) : (T)0;
+          }
+      __syncthreads();
+
+      const T teleport = (T)((1.0 - prm.alpha) * uni);  // (1-alpha)*uniform, :140
+      double r_old = 1.0;
+      int it_done = prm.max_iter;
+      bool converged = false;
+
+      for (int it = 1; it <= prm.max_iter; it++) {
+        // ---- phase U: u = z_A^T X (columns 0..N-1), g = X z_B (column N),
+        //      u[N] = z_A^T X z_B
+        for (int q = tid; q < 2 * N; q += NT) {
+          if (q < N) {
+            T su = 0;
+            for (int e = 0; e < nzAv; e++) su += Xs[zA[e] * P + q];
+            uS[q] = su;
+          } else {
+            const int i = q - N;
+            T sg = 0;
+            for (int e = 0; e < nzBv; e++) sg += Xs[i * P + zB[e]];
+            Xs[i * P + N] = sg;
+          }
+        }
+        if (warp == NW - 1) {
+          T s = 0;
+          const int tot = nzAv * nzBv;
+          for (int q = lane; q < tot; q += 32) {
+            const int e = q / nzBv, f = q - (q / nzBv) * nzBv;
+            s += Xs[zA[e] * P + zB[f]];
+          }
+#pragma unroll
+          for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+          if (lane == 0) uS[N] = s;
+        }
+        __syncthreads();
+
+        // ---- phase A: Y[k, j] = sum_e wA[e][k-k0] X[i_e, j] + u[j]/N, j in [0, N]
+        {
+          T ucol[KB];
+#pragma unroll
+          for (int c = 0; c < KB; c++) ucol[c] = uS[lane + 32 * c] * (T)invN;
+          for (int t = warp; t < KT; t += NW) {
+            T acc[KB][R];
+#pragma unroll
+            for (int c = 0; c < KB; c++)
+#pragma unroll
+              for (int r = 0; r < R; r++) acc[c][r] = 0;
+            const int e1 = toffA[t + 1];
+#pragma unroll 2
+            for (int e = toffA[t]; e < e1; e++) {
+              const int ioff = idxA[e];
+              T w[R];
+              load_w<T, R>(wA + e * R, w);
+#pragma unroll
+              for (int c = 0; c < KB; c++) {
+                const T x = Xs[ioff + lane + 32 * c];
+#pragma unroll
+                for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], x, acc[c][r]);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+              const int k = t * R + r;
+              if (k < N) {
+#pragma unroll
+                for (int c = 0; c < KB; c++) {
+                  const int j = lane + 32 * c;
+                  if (j <= N) Ys[k * P + j] = acc[c][r] + ucol[c];
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+
+        // ---- phase B: F[k, l] for owned tiles; reductions
+        const T alpha_eff = (T)(prm.alpha * r_old);
+        T sl = 0, dl = 0, ml = 0;
+        {
+          T vrow[KB];
+#pragma unroll
+          for (int c = 0; c < KB; c++) {
+            const int k = lane + 32 * c;
+            vrow[c] = (k < N) ? Ys[k * P + N] * (T)invN : (T)0;
+          }
+          const T rold = (T)r_old;
+#pragma unroll
+          for (int m = 0; m < MAXT; m++) {
+            const int t = warp + m * NW;
+            if (t < KT) {
+              T acc[KB][R];
+#pragma unroll
+              for (int c = 0; c < KB; c++)
+#pragma unroll
+                for (int r = 0; r < R; r++) acc[c][r] = 0;
+              const int e1 = toffB[t + 1];
+#pragma unroll 2
+              for (int e = toffB[t]; e < e1; e++) {
+                const int j = idxB[e];
+                T w[R];
+                load_w<T, R>(wB + e * R, w);
+#pragma unroll
+                for (int c = 0; c < KB; c++) {
+                  const T y = Ys[(lane + 32 * c) * P + j];
+#pragma unroll
+                  for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], y, acc[c][r]);
+                }
+              }
+#pragma unroll
+              for (int c = 0; c < KB; c++) {
+                const int k = lane + 32 * c;
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                  const int l = t * R + r;
+                  if (k < N && l < N) {
+                    const T f = fma(alpha_eff, acc[c][r] + vrow[c], teleport);
+                    const T diff = fma(-xold[m][c][r], rold, f);
+                    sl += f;
+                    dl += fabs(diff);
+                    ml += copysign(f, diff);
+                    xold[m][c][r] = f;
+                    Xs[k * P + l] = f;
+                  }
+                }
+              }
+            }
+          }
+        }
+        // block reduction in a fixed order (deterministic, no atomics)
+        double s3[3] = {(double)sl, (double)dl, (double)ml};
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+#pragma unroll
+          for (int m = 16; m > 0; m >>= 1) s3[q] += shfl_xor_d(s3[q], m);
+        if (lane == 0) {
+          red[warp * 3 + 0] = s3[0];
+          red[warp * 3 + 1] = s3[1];
+          red[warp * 3 + 2] = s3[2];
+        }
+        __syncthreads();
+        double s = 0, dp = 0, mm = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+          s += red[w * 3 + 0];
+          dp += red[w * 3 + 1];
+          mm += red[w * 3 + 2];
+        }
+        const double r = 1.0 / s;  // fresh /= fresh.sum(), :141
+        const double delta = dp + (r - 1.0) * mm;  // sum |fresh - x|, :142
+        r_old = r;
+        if (delta < prm.tol) {  // :144
+          it_done = it;
+          converged = true;
+          break;
+        }
+      }
+
+      // ---- epilogue: normalised X into Xs, greedy matching (similarity.py:96-108)
+      {
+        const T rr = (T)r_old;
+#pragma unroll
+        for (int m = 0; m < MAXT; m++)
+#pragma unroll
+          for (int c = 0; c < KB; c++)
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+              const int k = lane + 32 * c, l = (warp + m * NW) * R + r;
+              if (k < N && l < N) Xs[k * P + l] = xold[m][c][r] * rr;
+            }
+      }
+      __syncthreads();
+      // row maxima (value desc, column asc), cached in Ys scratch
+      T *rmv = Ys;
+      int32_t *rmc = (int32_t *)(Ys + (N + 32));
+      int32_t *mS = rmc + (N + 32);
+      for (int i = warp; i < N; i += NW) {
+        T bv = (T)-1;
+        int bc = 0x7fffffff;
+#pragma unroll
+        for (int c = 0; c < KB; c++) {
+          const int j = lane + 32 * c;
+          if (j < N) {
+            const T v = Xs[i * P + j];
+            if (v > bv) { bv = v; bc = j; }
+          }
+        }
+        warp_argmax(bv, bc);
+        if (lane == 0) { rmv[i] = bv; rmc[i] = bc; }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        bool active[KB], taken[KB];
+#pragma unroll
+        for (int c = 0; c < KB; c++) {
+          active[c] = (lane + 32 * c) < N;
+          taken[c] = (lane + 32 * c) >= N;
+        }
+        for (int round = 0; round < N; round++) {
+          T bv = (T)-2;
+          int brow = 0x7fffffff;
+#pragma unroll
+          for (int c = 0; c < KB; c++) {
+            const int i = lane + 32 * c;
+            if (active[c]) {
+              const T v = rmv[i];
+              if (v > bv || (v == bv && i < brow)) { bv = v; brow = i; }
+            }
+          }
+          warp_argmax(bv, brow);
+          const int bcol = rmc[brow];
+          if (lane == 0) mS[brow] = bcol;
+#pragma unroll
+          for (int c = 0; c < KB; c++) {
+            if (lane + 32 * c == brow) active[c] = false;
+            if (lane + 32 * c == bcol) taken[c] = true;
+          }
+          __syncwarp();
+          // rows whose cached argmax column was just taken: recompute
+#pragma unroll
+          for (int c = 0; c < KB; c++) {
+            const int i = lane + 32 * c;
+            unsigned bal = __ballot_sync(0xffffffffu, active[c] && rmc[i] == bcol);
+            while (bal) {
+              const int q = __ffs(bal) - 1 + 32 * c;
+              bal &= bal - 1;
+              T qv = (T)-1;
+              int qc = 0x7fffffff;
+#pragma unroll
+              for (int c2 = 0; c2 < KB; c2++) {
+                const int j = lane + 32 * c2;
+                if (!taken[c2]) {
+                  const T v = Xs[q * P + j];
+                  if (v > qv) { qv = v; qc = j; }
+                }
+              }
+              warp_argmax(qv, qc);
+              if (lane == 0) { rmv[q] = qv; rmc[q] = qc; }
+              __syncwarp();
+            }
+          }
+        }
+        __syncwarp();
+        // W = sum_i X[i, match(i)] (similarity.py:150), fixed-order tree
+        double wsum = 0.0;
+#pragma unroll
+        for (int c = 0; c < KB; c++) {
+          const int i = lane + 32 * c;
+          if (i < N) wsum += (double)Xs[i * P + mS[i]];
+        }
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) wsum += shfl_xor_d(wsum, m);
+        if (lane == 0) {
+          double dist;  // similarity.py:160-173
+          if (N == 1) {
+            dist = 1.0;
+          } else {
+            double cn = (wsum - 1.0 / N) / (1.0 - 1.0 / N);
+            cn = fmin(1.0, fmax(0.0, cn));
+            dist = 1.0 + (1.0 - cn);
+          }
+          if (out.d) out.d[slot] = dist;
+          if (out.W) out.W[slot] = wsum;
+          if (out.iters) out.iters[slot] = it_done;
+          if (out.conv) out.conv[slot] = converged ? 1 : 0;
+        }
+        if (out.match)
+          for (int i = lane; i < N; i += 32) out.match[i] = mS[i];
+      }
+      if (out.X)
+        for (int e = tid; e < N * N; e += NT) out.X[e] = (double)Xs[(e / N) * P + (e % N)];
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace cfgsim

@@ -1,0 +1,217 @@
+"""IsoRank pair similarity — drop-in for the reference's ISO path.
+
+Same names, signatures, defaults and error behaviour as
+``pkg/src/sasscfg/similarity.py``; every alignment runs in the sm_100a
+kernel (``csrc/isorank.cuh``) through the C ABI (``include/cfgsim.h``).
+
+Additions (keyword-only, defaults reproduce the reference):
+  precision="fp64"|"fp32"   fp64 reproduces the reference; fp32 stops on
+                            delta < max(tol, tol_fp32)
+  symmetric=True            pairwise ISO: one alignment per unordered pair,
+                            d(j,i) := d(i,j) (ISO is symmetric);
+                            False runs both directions like the reference
+  device=None               GPU ordinal (default: LOCAL_RANK or 0)
+and ``nearest`` (query-vs-corpus best match, no reference equivalent).
+
+The five flat measures (euc/man/min/jac/cos) are outside this round's hot
+path and raise NotImplementedError here.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .corpus import DeviceCorpus, pack
+from .errors import DegenerateInput, DimMismatch, DuplicateKernel
+from .matrix import TransitionMatrix
+
+
+class MeasureId(str, Enum):
+    EUC = "euc"
+    ISO = "iso"
+    MAN = "man"
+    MIN = "min"
+    JAC = "jac"
+    COS = "cos"
+
+
+@dataclass(frozen=True)
+class AlignmentResult:
+    """Node-pair alignment between two equal-size graphs (``similarity.py:69-82``)."""
+
+    matrix: np.ndarray
+    matching: tuple[int, ...]
+    matched_weight: float
+    iterations: int
+    converged: bool
+
+
+@dataclass(frozen=True)
+class PairwiseMatrix:
+    measure: MeasureId
+    kernel_ids: tuple[str, ...]
+    scores: np.ndarray
+    scaled: bool = False
+
+
+def _dev(device):
+    return nat.default_device() if device is None else int(device)
+
+
+def _check_alpha(alpha: float) -> None:
+    if not 0.0 < alpha < 1.0:  # similarity.py:129-130
+        raise ValueError(f"alpha must be in (0, 1), got {alpha}")
+
+
+def isorank_align(a: TransitionMatrix, b: TransitionMatrix, alpha: float = 0.85, tol: float = 1e-9,
+                  max_iter: int = 1000, start: np.ndarray | None = None, *, precision: str = "fp64",
+                  device: int | None = None) -> AlignmentResult:
+    """Damped power iteration on the Kronecker product (``similarity.py:111-157``)."""
+    if a.n != b.n:
+        raise DimMismatch(f"matrix dimensions differ: {a.n} vs {b.n}")
+    _check_alpha(alpha)
+    n = a.n
+    x0 = None
+    if start is not None:  # similarity.py:135
+        x0 = np.ascontiguousarray(np.asarray(start, dtype=float) / np.sum(start), dtype=np.float64)
+        if x0.size != n * n:
+            raise DimMismatch(f"start vector has {x0.size} entries, expected {n * n}")
+    A = np.ascontiguousarray(a.entries, dtype=np.float64)
+    B = np.ascontiguousarray(b.entries, dtype=np.float64)
+    X = np.empty((n, n))
+    m = np.empty(n, np.int32)
+    d = np.empty(1)
+    w = np.empty(1)
+    it = np.empty(1, np.int32)
+    cv = np.empty(1, np.uint8)
+    prm = nat.params(alpha, tol, max_iter, precision)
+    nat.check(nat.lib.cfgsim_isorank_single(_dev(device), n, nat.ptr(A), n, nat.ptr(B), nat.C.byref(prm),
+                                            nat.ptr(x0), nat.ptr(X), nat.ptr(m), nat.ptr(d), nat.ptr(w),
+                                            nat.ptr(it), nat.ptr(cv)))
+    return AlignmentResult(matrix=X, matching=tuple(int(v) for v in m), matched_weight=float(w[0]),
+                           iterations=int(it[0]), converged=bool(cv[0]))
+
+
+def isorank_distance(alignment: AlignmentResult) -> float:
+    """Distance in [1, 2] from the matched weight (``similarity.py:160-173``)."""
+    n = alignment.matrix.shape[0]
+    if n == 1:
+        return 1.0
+    conc = (alignment.matched_weight - 1.0 / n) / (1.0 - 1.0 / n)
+    conc = min(1.0, max(0.0, conc))
+    return 1.0 + (1.0 - conc)
+
+
+def measure_distance(a: TransitionMatrix, b: TransitionMatrix, measure: MeasureId, *, p: float = 3.0,
+                     alpha: float = 0.85, tol: float = 1e-9, max_iter: int = 1000,
+                     precision: str = "fp64", device: int | None = None) -> float:
+    """Size-normalise a pair and apply one measure (``similarity.py:176-200``).
+
+    For ISO the size normalisation (``normalize_pair``) is fused into the
+    kernel prologue."""
+    if measure is not MeasureId.ISO:
+        if measure in tuple(MeasureId):
+            raise NotImplementedError(f"measure {measure.value!r} is not on this build's hot path")
+        raise ValueError(f"unknown measure {measure!r}")
+    _check_alpha(alpha)
+    A = np.ascontiguousarray(a.entries, dtype=np.float64)
+    B = np.ascontiguousarray(b.entries, dtype=np.float64)
+    d = np.empty(1)
+    prm = nat.params(alpha, tol, max_iter, precision)
+    nat.check(nat.lib.cfgsim_isorank_single(_dev(device), a.n, nat.ptr(A), b.n, nat.ptr(B), nat.C.byref(prm),
+                                            None, None, None, nat.ptr(d), None, None, None))
+    return float(d[0])
+
+
+def pairwise(matrices: list[TransitionMatrix], measure: MeasureId, *, p: float = 3.0, alpha: float = 0.85,
+             tol: float = 1e-9, max_iter: int = 1000, precision: str = "fp64", symmetric: bool = True,
+             device: int | None = None, return_iterations: bool = False):
+    """All-pairs scores ordered by kernel_id (``similarity.py:211-257``).
+
+    ISO fills the diagonal and both directions.  The whole corpus is packed
+    and uploaded once; all alignments run in persistent sm_100a kernels."""
+    if len(matrices) < 2:
+        raise ValueError("pairwise comparison needs at least 2 kernels")
+    ordered = sorted(matrices, key=lambda m: m.kernel_id)
+    ids = tuple(m.kernel_id for m in ordered)
+    if len(set(ids)) != len(ids):
+        raise DuplicateKernel("duplicate kernel_id in pairwise input")
+    if measure is not MeasureId.ISO:
+        if measure in tuple(MeasureId):
+            raise NotImplementedError(f"measure {measure.value!r} is not on this build's hot path")
+        raise ValueError(f"unknown measure {measure!r}")
+    _check_alpha(alpha)
+    k = len(ordered)
+    scores = np.empty((k, k))
+    iters = np.empty((k, k), np.int32) if return_iterations else None
+    prm = nat.params(alpha, tol, max_iter, precision)
+    with DeviceCorpus(pack(ordered), _dev(device)) as corpus:
+        nat.check(nat.lib.cfgsim_allpairs(corpus.handle, 0 if symmetric else 1, nat.C.byref(prm),
+                                          nat.ptr(scores), nat.ptr(iters), None))
+    pm = PairwiseMatrix(measure=measure, kernel_ids=ids, scores=scores, scaled=False)
+    return (pm, iters) if return_iterations else pm
+
+
+def minmax_scale(pm: PairwiseMatrix) -> PairwiseMatrix:
+    """Affine rescale to [0, 1] over finite entries (``similarity.py:260-284``);
+    ISO's diagonal takes part, the flat measures' zero diagonal does not."""
+    k = pm.scores.shape[0]
+    mask = np.isfinite(pm.scores)
+    if pm.measure is not MeasureId.ISO:
+        mask &= ~np.eye(k, dtype=bool)
+    picked = pm.scores[mask]
+    if picked.size == 0:
+        raise DegenerateInput("no finite entries to scale")
+    lo, hi = float(picked.min()), float(picked.max())
+    out = pm.scores.copy()
+    out[mask] = 0.0 if hi == lo else (pm.scores[mask] - lo) / (hi - lo)
+    return PairwiseMatrix(measure=pm.measure, kernel_ids=pm.kernel_ids, scores=out, scaled=True)
+
+
+def export_heatmap_csv(pm: PairwiseMatrix) -> str:
+    """CSV, kernel_id header row/column, 6 decimals, ``nan`` (``similarity.py:287-293``)."""
+    header = "," + ",".join(pm.kernel_ids)
+    body = [
+        kid + "," + ",".join(f"{v:.6f}" if np.isfinite(v) else "nan" for v in row)
+        for kid, row in zip(pm.kernel_ids, pm.scores)
+    ]
+    return "\n".join([header, *body]) + "\n"
+
+
+def nearest(queries: Sequence[TransitionMatrix], corpus: Sequence[TransitionMatrix], *, alpha: float = 0.85,
+            tol: float = 1e-9, max_iter: int = 1000, precision: str = "fp64",
+            device: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Best match of every query in ``corpus``: ``argmin_j measure_distance(q,
+    corpus[j], ISO)``, ties to the lowest j.  Returns (best_d, best_index)."""
+    _check_alpha(alpha)
+    dev = _dev(device)
+    nq = len(queries)
+    best_d = np.empty(nq)
+    best_i = np.empty(nq, np.int64)
+    prm = nat.params(alpha, tol, max_iter, precision)
+    with DeviceCorpus(pack(queries), dev) as Q, DeviceCorpus(pack(corpus), dev) as Cc:
+        nat.check(nat.lib.cfgsim_nearest(Q.handle, Cc.handle, 0, Cc.K, nat.C.byref(prm), nat.ptr(best_d),
+                                         nat.ptr(best_i), None))
+    return best_d, best_i
+
+
+def isorank_pairs(A: DeviceCorpus, B: DeviceCorpus, ia, ib, *, alpha: float = 0.85, tol: float = 1e-9,
+                  max_iter: int = 1000, precision: str = "fp64", stream=None):
+    """Batched ``measure_distance(A[ia[p]], B[ib[p]], ISO)``: returns (d, W, iters, converged)."""
+    _check_alpha(alpha)
+    ia = np.ascontiguousarray(ia, np.int32)
+    ib = np.ascontiguousarray(ib, np.int32)
+    n = len(ia)
+    d = np.empty(n)
+    w = np.empty(n)
+    it = np.empty(n, np.int32)
+    cv = np.empty(n, np.uint8)
+    prm = nat.params(alpha, tol, max_iter, precision)
+    nat.check(nat.lib.cfgsim_isorank_pairs(A.handle, B.handle, n, nat.ptr(ia), nat.ptr(ib), nat.C.byref(prm),
+                                           nat.ptr(d), nat.ptr(w), nat.ptr(it), nat.ptr(cv), stream))
+    return d, w, it, cv.astype(bool)

@@ -1,0 +1,256 @@
+"""Parity of the sm_100a IsoRank path against the reference (golden vectors)
+and the pinned CPU oracle.  Runs on the B200 box (``-m gpu``).
+
+Bar (BASELINE.json north_star): fp64 — identical iteration counts, distance
+within 1e-9 relative (observed ~1e-15); fp32 — distance within 1e-5.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden, unravel
+
+pytestmark = pytest.mark.gpu
+
+RTOL64 = 1e-9
+RTOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def P(gpu):
+    import paper_1707_02423_b200 as P
+    return P
+
+
+def mat(P, e, kid="r.synth.t.rand"):
+    e = np.asarray(e, float)
+    return P.TransitionMatrix(kid, e, tuple(range(len(e))), P.RAW_COUNTS)
+
+
+# ------------------------------------------------------------ interpolation
+def test_interpolate_bit_exact(P):
+    g = load_golden("interp.npz")
+    srcs, outs = unravel(g["ss"], g["fs"]), unravel(g["so"], g["fo"])
+    for src, t, out in zip(srcs, g["targets"], outs):
+        m = mat(P, src)
+        got = P.interpolate_to(m, int(t))
+        if int(t) == src.shape[0]:
+            assert got is m  # matrix.py:85-86
+        np.testing.assert_array_equal(got.entries, out)
+
+
+# ------------------------------------------------------------ single pairs
+def test_small_pairs_against_reference(P):
+    g = load_golden("small_pairs.npz")
+    A, B, X = unravel(g["sa"], g["fa"]), unravel(g["sb"], g["fb"]), unravel(g["sx"], g["fx"])
+    for i, (a, b) in enumerate(zip(A, B)):
+        d = P.measure_distance(mat(P, a), mat(P, b), P.MeasureId.ISO)
+        assert d == pytest.approx(g["d"][i], rel=1e-12, abs=1e-12), i
+        if g["same"][i]:
+            al = P.isorank_align(mat(P, a), mat(P, b))
+            assert al.iterations == g["iters"][i]
+            assert al.converged == g["converged"][i]
+            np.testing.assert_allclose(al.matrix, X[i], rtol=1e-10, atol=1e-15)
+            assert al.matched_weight == pytest.approx(g["W"][i], rel=1e-12)
+            assert sorted(al.matching) == list(range(a.shape[0]))
+
+
+def test_reference_pinned_cases(P):
+    s = load_golden("special.npz")
+    al = P.isorank_align(mat(P, [[0.0]]), mat(P, [[0.0]]))  # test_similarity.py:150-155
+    np.testing.assert_array_equal(al.matrix, [[1.0]])
+    assert al.matching == (0,) and al.matched_weight == 1.0
+    assert al.converged and al.iterations == 1
+    al = P.isorank_align(mat(P, np.zeros((3, 3))), mat(P, np.zeros((3, 3))))  # :191-195
+    assert al.matching == (0, 1, 2)
+    al = P.isorank_align(mat(P, s["small_alpha_a"]), mat(P, s["small_alpha_b"]), alpha=1e-9)  # :176-181
+    np.testing.assert_allclose(al.matrix, np.full((3, 3), 1.0 / 9.0), atol=1e-8)
+    assert al.matched_weight == pytest.approx(1.0 / 3.0, abs=1e-8)
+    al = P.isorank_align(mat(P, s["start_a"]), mat(P, s["start_b"]), start=s["start_vec"])  # :183-189
+    np.testing.assert_allclose(al.matrix, s["start_X"], rtol=1e-10)
+    assert al.iterations == s["start_iters"]
+    for c in range(1, 8):  # :167-174
+        al = P.isorank_align(mat(P, s["cut_a"]), mat(P, s["cut_b"]), max_iter=c)
+        assert al.iterations == c
+        assert (al.matrix >= 0).all()
+        assert al.matrix.sum() == pytest.approx(1.0, abs=1e-9)
+        np.testing.assert_allclose(al.matrix, s["cut_X"][c - 1], rtol=1e-12)
+    rng = np.random.default_rng(95)  # :204-208
+    al = P.isorank_align(mat(P, rng.random((2, 2))), mat(P, rng.random((2, 2))), max_iter=1)
+    assert not al.converged and al.iterations == 1
+
+
+def test_uniform_alignment_scores_two(P):  # test_similarity.py:242-244
+    al = P.isorank_align(mat(P, np.zeros((4, 4))), mat(P, np.zeros((4, 4))), alpha=1e-9)
+    assert P.isorank_distance(al) == pytest.approx(2.0, abs=1e-6)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 1.0, 1.2, -0.1])
+def test_alpha_range_enforced(P, alpha):
+    with pytest.raises(ValueError):
+        P.isorank_align(mat(P, np.eye(2)), mat(P, np.eye(2)[::-1]), alpha=alpha)
+
+
+def test_dim_mismatch(P):
+    with pytest.raises(P.DimMismatch):
+        P.isorank_align(mat(P, [[1.0]]), mat(P, np.eye(2)))
+
+
+def test_measure_distance_normalises_sizes(P):  # test_similarity.py:260-263
+    rng = np.random.default_rng(8)
+    d = P.measure_distance(mat(P, rng.random((2, 2))), mat(P, rng.random((3, 3))), P.MeasureId.ISO)
+    assert 1.0 <= d <= 2.0
+
+
+# ------------------------------------------------------------ synthetic CFG pairs (batched path)
+def test_synthetic_cfg_pairs_against_reference(P):
+    g = load_golden("synth_pairs.npz")
+    A, B = unravel(g["sa"], g["fa"]), unravel(g["sb"], g["fb"])
+    n = len(A)
+    with P.DeviceCorpus(A) as CA, P.DeviceCorpus(B) as CB:
+        d, w, it, cv = P.isorank_pairs(CA, CB, np.arange(n), np.arange(n))
+    np.testing.assert_array_equal(it, g["iters"])
+    np.testing.assert_allclose(d, g["d"], rtol=1e-12)
+    np.testing.assert_allclose(w, g["W"], rtol=1e-10)
+    assert cv.all()
+
+
+# ------------------------------------------------------------ config 1: bundled corpus
+def _bundled(P):
+    g = load_golden("bundled_corpus.npz")
+    mats = unravel(g["sizes"], g["flat"])
+    # shuffled input order: pairwise must sort by kernel_id (similarity.py:229)
+    tms = [P.TransitionMatrix(str(k), m, tuple(range(len(m))), P.ROW_STOCHASTIC) for k, m in zip(g["ids"], mats)]
+    return g, tms[::-1]
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_bundled_corpus_pairwise(P, symmetric):
+    g, tms = _bundled(P)
+    pm, iters = P.pairwise(tms, P.MeasureId.ISO, symmetric=symmetric, return_iterations=True)
+    assert pm.kernel_ids == tuple(str(x) for x in g["ids"])
+    np.testing.assert_allclose(pm.scores, g["scores"], rtol=1e-12)
+    if not symmetric:
+        np.testing.assert_array_equal(iters, g["iters"])
+    else:
+        np.testing.assert_array_equal(np.triu(iters), np.triu(g["iters"]))
+
+
+def test_bundled_corpus_csv_byte_identical(P):
+    g, tms = _bundled(P)
+    pm = P.pairwise(tms, P.MeasureId.ISO, symmetric=False)
+    assert P.export_heatmap_csv(pm) == (GOLDEN / "iso.csv").read_text()
+    assert P.export_heatmap_csv(P.minmax_scale(pm)) == (GOLDEN / "iso_scaled.csv").read_text()
+
+
+def test_pairwise_errors(P):
+    with pytest.raises(ValueError):
+        P.pairwise([mat(P, [[1.0]])], P.MeasureId.ISO)
+    with pytest.raises(P.DuplicateKernel):
+        P.pairwise([mat(P, [[1.0]], "x.s.t.d"), mat(P, [[2.0]], "x.s.t.d")], P.MeasureId.ISO)
+
+
+# ------------------------------------------------------------ config-2-like sample vs the C oracle
+@pytest.fixture(scope="module")
+def c2_sample(P):
+    from paper_1707_02423_b200 import synth
+    mats = synth.random_corpus(96, 16, 64, seed=5)
+    return mats
+
+
+def test_allpairs_sample_matches_oracle(P, c2_sample):
+    from oracle import ffi
+    mats = c2_sample
+    k = len(mats)
+    tms = [P.TransitionMatrix(f"g{i:04d}", m, tuple(range(len(m))), P.ROW_STOCHASTIC) for i, m in enumerate(mats)]
+    pm, iters = P.pairwise(tms, P.MeasureId.ISO, return_iterations=True)
+    iu, ju = np.triu_indices(k)
+    d, w, it, cv = ffi.iso_batch(P.pack(mats), iu.astype(np.int32), ju.astype(np.int32))
+    np.testing.assert_allclose(pm.scores[iu, ju], d, rtol=RTOL64)
+    mism = int((iters[iu, ju] != it).sum())
+    assert mism == 0, f"{mism} iteration-count mismatches of {len(iu)}"
+    np.testing.assert_array_equal(pm.scores, pm.scores.T)
+
+
+def test_fp32_mode_within_tolerance(P, c2_sample):
+    from oracle import ffi
+    mats = c2_sample[:40]
+    k = len(mats)
+    tms = [P.TransitionMatrix(f"g{i:04d}", m, tuple(range(len(m))), P.ROW_STOCHASTIC) for i, m in enumerate(mats)]
+    pm = P.pairwise(tms, P.MeasureId.ISO, precision="fp32")
+    iu, ju = np.triu_indices(k)
+    d, *_ = ffi.iso_batch(P.pack(mats), iu.astype(np.int32), ju.astype(np.int32))
+    np.testing.assert_allclose(pm.scores[iu, ju], d, rtol=RTOL32)
+
+
+def test_deterministic_and_path_independent(P, c2_sample):
+    mats = c2_sample[:48]
+    tms = [P.TransitionMatrix(f"g{i:04d}", m, tuple(range(len(m))), P.ROW_STOCHASTIC) for i, m in enumerate(mats)]
+    a = P.pairwise(tms, P.MeasureId.ISO).scores
+    b = P.pairwise(tms, P.MeasureId.ISO).scores
+    np.testing.assert_array_equal(a, b)
+    iu, ju = np.triu_indices(len(mats))
+    with P.DeviceCorpus(mats) as C:
+        d, *_ = P.isorank_pairs(C, C, iu, ju)
+    # the same pair through the list path and the triangle path: bitwise equal
+    np.testing.assert_array_equal(d, a[iu, ju])
+
+
+def test_nearest_matches_oracle(P, c2_sample):
+    from oracle import ffi
+    q = c2_sample[:6]
+    corpus = c2_sample[6:60]
+    bd, bi = P.nearest(q, corpus)
+    allm = q + corpus
+    packed = P.pack(allm)
+    for i in range(len(q)):
+        ia = np.full(len(corpus), i, np.int32)
+        ib = np.arange(len(q), len(allm), dtype=np.int32)
+        d, *_ = ffi.iso_batch(packed, ia, ib)
+        assert bi[i] == int(np.argmin(d))
+        assert bd[i] == pytest.approx(d.min(), rel=RTOL64)
+
+
+# ------------------------------------------------------------ tiers and edge cases
+def test_large_tier_pairs(P):
+    from oracle import ffi
+    from paper_1707_02423_b200 import synth
+    mats = synth.random_corpus(8, 70, 104, seed=9)
+    with P.DeviceCorpus(mats) as C:
+        ia = np.arange(0, 8, 2)
+        ib = ia + 1
+        d, w, it, cv = P.isorank_pairs(C, C, ia, ib)
+    for k in range(len(ia)):
+        r = ffi.iso_pair(mats[ia[k]], mats[ib[k]])
+        assert it[k] == r["iterations"]
+        assert d[k] == pytest.approx(r["d"], rel=RTOL64)
+
+
+def test_dense_operators_overflow_path(P):
+    """Dense random operators exceed the typical list capacity and are re-run
+    with dense-bound lists; results must not change."""
+    from oracle import ffi
+    rng = np.random.default_rng(3)
+    mats = [rng.random((n, n)) for n in (40, 55, 63, 20, 31, 47)]
+    with P.DeviceCorpus(mats) as C:
+        ia = np.array([0, 1, 2, 3, 4, 5, 0], np.int32)
+        ib = np.array([1, 2, 3, 4, 5, 0, 0], np.int32)
+        d, w, it, cv = P.isorank_pairs(C, C, ia, ib)
+    for k in range(len(ia)):
+        r = ffi.iso_pair(mats[ia[k]], mats[ib[k]])
+        assert it[k] == r["iterations"]
+        assert d[k] == pytest.approx(r["d"], rel=RTOL64)
+
+
+def test_degenerate_graphs(P):
+    from oracle import ffi
+    rng = np.random.default_rng(4)
+    cases = [(np.zeros((1, 1)), rng.random((5, 5))), (np.ones((1, 1)) * 3, rng.random((7, 7))),
+             (np.zeros((6, 6)), np.zeros((9, 9))), (np.eye(33), np.eye(33)[::-1].copy()),
+             (np.zeros((64, 64)), rng.random((2, 2)))]
+    for a, b in cases:
+        d = P.measure_distance(mat(P, a), mat(P, b), P.MeasureId.ISO)
+        r = ffi.iso_pair(a, b)
+        assert d == pytest.approx(r["d"], rel=RTOL64)
