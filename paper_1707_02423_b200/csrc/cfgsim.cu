@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -20,6 +21,7 @@
 
 #include "../../include/cfgsim.h"
 #include "isorank.cuh"
+#include "tiers.h"
 
 using namespace cfgsim;
 
@@ -99,7 +101,7 @@ namespace {
 
 // ---------------------------------------------------------------- tiers
 // A tier is one kernel instantiation.  nmax is the largest N it can hold
-// on-chip (lanes cover N+1 columns in phase A).  occ is the CTAs/SM the
+// on-chip (phase A handles column N = 32*KB with an extra uniform pass).  occ is the CTAs/SM the
 // tier is tuned for (register-limited); the list capacity is whatever
 // shared memory is left at that occupancy, capped by the dense bound.
 struct Tier {
@@ -113,7 +115,7 @@ struct Tier {
 template <typename T, int KB, int NW, int R, int MINB>
 Tier make_tier() {
   Tier t;
-  t.nmax = 32 * KB - 1;
+  t.nmax = 32 * KB;
   t.kb = KB;
   t.nw = NW;
   t.r = R;
@@ -125,9 +127,10 @@ Tier make_tier() {
 }
 
 const std::vector<Tier> &tiers(int precision) {
-  static std::vector<Tier> t64 = {make_tier<double, 1, 4, 4, 5>(), make_tier<double, 2, 8, 4, 2>(),
+  // R = 4 row/column tiles (measured faster than R = 2 on config-2 corpora)
+  static std::vector<Tier> t64 = {make_tier<double, 1, 4, 4, 6>(), make_tier<double, 2, 8, 4, 3>(),
                                   make_tier<double, 4, 16, 4, 1>()};
-  static std::vector<Tier> t32 = {make_tier<float, 1, 4, 4, 5>(), make_tier<float, 2, 8, 4, 2>(),
+  static std::vector<Tier> t32 = {make_tier<float, 1, 4, 4, 6>(), make_tier<float, 2, 8, 4, 3>(),
                                   make_tier<float, 4, 16, 4, 1>()};
   return precision == CFGSIM_FP32 ? t32 : t64;
 }
@@ -137,29 +140,65 @@ constexpr size_t kSmemPerSM = 228 * 1024; // per SM, incl. 1 KB reserved per CTA
 
 int dense_cap(int nlim, int r) { return ((nlim + r - 1) / r) * nlim; }
 
-// list capacity for a launch of tier T sized for nlim; dense -> dense bound
-int plan_cap(const Tier &T, int nlim, bool dense) {
-  const int dc = dense_cap(nlim, T.r);
-  const size_t base = T.smem(nlim, 0) + 64;
-  if (dense) return (T.smem(nlim, dc) <= kMaxSmem) ? dc : -1;
-  const size_t budget = std::min(kMaxSmem, kSmemPerSM / T.occ - 1024);
-  if (base >= budget) return (T.smem(nlim, std::min(dc, 4 * nlim)) <= kMaxSmem) ? std::min(dc, 4 * nlim) : -1;
-  const int cap = (int)((budget - base) / (2 * T.entry_bytes)) - 8;
-  return std::max(1, std::min(cap, dc));
+// CTAs/SM a tier can reach with no dynamic smem (register / warp limits)
+int occ_limit(const Tier &T) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : cache)
+    if (e.first == T.fn) return e.second;
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, T.fn, T.nw * 32, 0) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  occ = std::max(1, occ);
+  cache.push_back({T.fn, occ});
+  return occ;
 }
 
-// smallest tier holding N whose smem fits; -1 if none
-int tier_index(int precision, int N, bool dense, int *cap_out) {
+struct Plan {
+  int ti = -1, cap = 0, occ = 0;
+  bool same_launch(const Plan &o) const { return ti == o.ti && occ == o.occ; }
+};
+
+// Tier, list capacity and target CTAs/SM for pairs of size N.  Typical CFG
+// operators need <= ~5N list entries per side (measured on config-2
+// corpora); the capacity is whatever fits at the highest reachable
+// occupancy.  Pairs that still overflow are re-run with the dense bound.
+Plan plan_for(int precision, int N, bool dense) {
   const auto &ts = tiers(precision);
   for (size_t i = 0; i < ts.size(); i++) {
-    if (N > ts[i].nmax) continue;
-    const int cap = plan_cap(ts[i], N, dense);
-    if (cap > 0) {
-      *cap_out = cap;
-      return (int)i;
+    const Tier &T = ts[i];
+    if (N > T.nmax) continue;
+    const int dc = dense_cap(N, T.r);
+    const int need = dense ? dc : std::min(dc, 5 * N + 16);
+    const size_t base = T.smem(N, 0) + 64;
+    for (int occ = occ_limit(T); occ >= 1; occ--) {
+      const size_t budget = std::min(kMaxSmem, kSmemPerSM / occ - 1024);
+      if (base >= budget) continue;
+      const int fit = (int)((budget - base) / (2 * T.entry_bytes)) - 8;
+      if (fit >= need) {
+        Plan pl;
+        pl.ti = (int)i;
+        pl.cap = std::min(fit, dc);
+        pl.occ = occ;
+        return pl;
+      }
     }
   }
-  return -1;
+  return Plan{};
+}
+
+// capacity for a launch sized for nlim at the plan's occupancy
+int cap_for(int precision, const Plan &pl, int nlim, bool dense) {
+  const Tier &T = tiers(precision)[pl.ti];
+  const int dc = dense_cap(nlim, T.r);
+  if (dense) return dc;
+  const size_t base = T.smem(nlim, 0) + 64;
+  const size_t budget = std::min(kMaxSmem, kSmemPerSM / pl.occ - 1024);
+  if (base >= budget) return std::min(dc, 5 * nlim + 16);
+  return std::max(1, std::min(dc, (int)((budget - base) / (2 * T.entry_bytes)) - 8));
 }
 
 struct Scratch {
@@ -287,7 +326,7 @@ int handle_overflow(const cfgsim_corpus *A, const cfgsim_corpus *B, const PairWo
     const int a = (int)(std::upper_bound(rs.begin(), rs.end(), u) - rs.begin()) - 1;
     const int b = a + (int)(u - rs[a]);
     int g1 = A->perm[a], g2 = A->perm[b];
-    if (dir) std::swap(g1, g2);
+    if (work.ordered ? dir != 0 : g1 > g2) std::swap(g1, g2);
     ia.push_back(g1);
     ib.push_back(g2);
     sl.push_back(work.ordered ? 2 * (u - work.out_base) + dir : (u - work.out_base));
@@ -317,21 +356,26 @@ int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<i
   if (n == 0) return CFGSIM_OK;
   Scratch &S = scratch_for(A->device);
   if (int rc = ensure_scratch(S, 1 << 16)) return rc;
-  // bucket by tier, within a tier by descending N (largest first)
-  const int nt = (int)tiers(p->precision).size();
-  std::vector<std::vector<int64_t>> bucket(nt);
+  // bucket by launch plan (tier, occupancy), within a bucket by descending N
+  std::vector<Plan> plans;
+  std::vector<std::vector<int64_t>> bucket;
   for (int64_t q = 0; q < n; q++) {
     const int N = std::max(A->n_nodes[ia[q]], B->n_nodes[ib[q]]);
-    int cap;
-    const int ti = tier_index(p->precision, N, cap_mode != 0, &cap);
-    if (ti < 0)
+    const Plan pl = plan_for(p->precision, N, cap_mode != 0);
+    if (pl.ti < 0)
       return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
                                       " exceeds the on-chip tiers of this build");
-    bucket[ti].push_back(q);
+    size_t bi = 0;
+    while (bi < plans.size() && !plans[bi].same_launch(pl)) bi++;
+    if (bi == plans.size()) {
+      plans.push_back(pl);
+      bucket.emplace_back();
+    }
+    bucket[bi].push_back(q);
   }
-  for (int ti = 0; ti < nt; ti++) {
-    auto &bk = bucket[ti];
-    if (bk.empty()) continue;
+  for (size_t bi = 0; bi < bucket.size(); bi++) {
+    auto &bk = bucket[bi];
+    const int ti = plans[bi].ti;
     std::stable_sort(bk.begin(), bk.end(), [&](int64_t x, int64_t y) {
       return std::max(A->n_nodes[ia[x]], B->n_nodes[ib[x]]) >
              std::max(A->n_nodes[ia[y]], B->n_nodes[ib[y]]);
@@ -369,10 +413,9 @@ int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<i
     o.ovf_count = S.ovf_count.as<int32_t>();
     o.ovf_list = S.ovf_list.as<int64_t>();
     o.ovf_cap = (int32_t)S.ovf_cap;
-    const int cap2 = plan_cap(tiers(p->precision)[ti], nlim, cap_mode != 0);
-    if (cap2 < 1) return fail(CFGSIM_ERR_ARG, "no list capacity for this tier");
+    const int cap2 = cap_for(p->precision, plans[bi], nlim, cap_mode != 0);
     if (int rc = launch_tier(p->precision, ti, nlim, cap2, A->dev(), B->dev(), w, o, p,
-                             S.counters.as<unsigned long long>() + ti, st))
+                             S.counters.as<unsigned long long>() + (bi % 32), st))
       return rc;
     // overflowed items: rerun with dense-bound lists
     int32_t cnt = 0;
@@ -675,16 +718,16 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   int launch_no = 0;
   while (u < u1) {
     const int N = c->n_sorted[a];
-    int cap;
-    const int ti = tier_index(p->precision, N, false, &cap);
-    if (ti < 0)
+    const Plan pl = plan_for(p->precision, N, false);
+    if (pl.ti < 0)
       return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
                                       " exceeds the on-chip tiers of this build");
-    // extend over rows in the same tier
+    // extend over rows with the same launch plan (rows are sorted by n desc)
     int a_end = a;
-    int cap_e;
-    while (a_end + 1 < c->K && tier_index(p->precision, c->n_sorted[a_end + 1], false, &cap_e) == ti)
+    while (a_end + 1 < c->K && plan_for(p->precision, c->n_sorted[a_end + 1], false).same_launch(pl))
       a_end++;
+    const int ti = pl.ti;
+    const int cap = cap_for(p->precision, pl, N, false);
     const int64_t seg_end = std::min(u1, c->row_start[a_end + 1]);
     PairWork w{};
     w.mode = WORK_TRIANGLE;

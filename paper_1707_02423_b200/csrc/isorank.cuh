@@ -25,7 +25,7 @@
 //      reduce s = sum F, dp = sum |F - X_old|, m = sum sign(F - X_old) F
 //   delta = sum |F/s - X_old| = dp + (1/s - 1) m   (exact to first order in
 //   |1-s| ~ 1e-16), stop when delta < tol
-//   (similarity.py:141-146).  X_old lives in registers of its owner thread.
+//   (similarity.py:141-146).  X_old is re-read from Xs before F overwrites it.
 // Epilogue: greedy matching with cached row maxima (same tie rule as
 // similarity.py:96-108), W, d (similarity.py:150,160-173).
 #pragma once
@@ -88,7 +88,7 @@ __device__ __forceinline__ double shfl_xor_d(double v, int m) { return __shfl_xo
 
 // numpy DOUBLE_pairwise_sum order (umath/loops_utils.h.src), stride 1 —
 // the order of `out.sum(axis=1)` in similarity.py:89.  One thread.
-__device__ double np_pairwise_leaf(const double *a, int n) {  // n <= 128
+__device__ inline double np_pairwise_leaf(const double *a, int n) {  // n <= 128
   if (n < 8) {
     double res = 0.;
     for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
@@ -110,7 +110,7 @@ __device__ double np_pairwise_leaf(const double *a, int n) {  // n <= 128
 
 // The recursion `pw(a, n2) + pw(a + n2, n - n2)` (n2 = n/2 rounded down to a
 // multiple of 8) unrolled with an explicit stack.
-__device__ double np_pairwise_sum(const double *a, int n) {
+__device__ inline double np_pairwise_sum(const double *a, int n) {
   if (n <= 128) return np_pairwise_leaf(a, n);
   int off[24], len[24], state[24];
   double left[24];
@@ -179,9 +179,78 @@ __device__ __forceinline__ void warp_argmax(T &v, int &idx) {
   }
 }
 
+// Total order of the reference's greedy matching inside one row:
+// larger value first, then lower column (np.argmax first occurrence).
+template <typename T>
+__device__ __forceinline__ bool before(T v1, int c1, T v2, int c2) {
+  return v1 > v2 || (v1 == v2 && c1 < c2);
+}
+
+// Warp-wide bitonic sort of 32*KB (value, column) pairs into `before` order;
+// element e = cc*32 + lane lives in v[cc], c[cc].
+template <typename T, int KB>
+__device__ __forceinline__ void warp_sort_desc(T (&v)[KB], int (&c)[KB], int lane) {
+  constexpr int n = 32 * KB;
+#pragma unroll
+  for (int k = 2; k <= n; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int cc = 0; cc < KB; cc++) {
+          const int pc = cc ^ (j >> 5);
+          if (pc > cc) {
+            const bool up = ((cc * 32 + lane) & k) == 0;
+            const bool sw = up ? before(v[pc], c[pc], v[cc], c[cc]) : before(v[cc], c[cc], v[pc], c[pc]);
+            if (sw) {
+              const T tv = v[cc]; v[cc] = v[pc]; v[pc] = tv;
+              const int tc = c[cc]; c[cc] = c[pc]; c[pc] = tc;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < KB; cc++) {
+          const T ov = __shfl_xor_sync(0xffffffffu, v[cc], j);
+          const int oc = __shfl_xor_sync(0xffffffffu, c[cc], j);
+          const bool lower = (lane & j) == 0;
+          const bool up = ((cc * 32 + lane) & k) == 0;
+          const bool take = (lower == up) ? before(ov, oc, v[cc], c[cc]) : before(v[cc], c[cc], ov, oc);
+          if (take) { v[cc] = ov; c[cc] = oc; }
+        }
+      }
+    }
+  }
+}
+
+// Phase A inner loop over one tile's entries: acc[c][r] += w_e[r] * X[i_e, lane+32c];
+// EXTRA also accumulates column xcol (= N when N == 32*KB) uniformly.
+template <typename T, int KB, int R, bool EXTRA>
+__device__ __forceinline__ void tile_accumulate_rows(const int32_t *__restrict__ idx, const T *__restrict__ wts,
+                                                     const T *__restrict__ Xs, int e0, int e1, int lane, int xcol,
+                                                     T (&acc)[KB][R], T (&accx)[R]) {
+#pragma unroll 2
+  for (int e = e0; e < e1; e++) {
+    const int ioff = idx[e];
+    T w[R];
+    load_w<T, R>(wts + e * R, w);
+#pragma unroll
+    for (int c = 0; c < KB; c++) {
+      const T x = Xs[ioff + lane + 32 * c];
+#pragma unroll
+      for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], x, acc[c][r]);
+    }
+    if (EXTRA) {
+      const T x = Xs[ioff + xcol];
+#pragma unroll
+      for (int r = 0; r < R; r++) accx[r] = fma(w[r], x, accx[r]);
+    }
+  }
+}
+
 // Shared-memory carve-up, identical on host and device.
 struct Smem {
-  size_t x, y, idxA, wA, idxB, wB, toffA, toffB, zA, zB, uS, lo, fr, zflag, red, misc, total;
+  size_t x, y, idxA, wA, idxB, wB, toffA, toffB, ordA, ordB, zA, zB, uS, lo, fr, zflag, red, misc, total;
 };
 
 template <typename T, int R>
@@ -204,6 +273,8 @@ __host__ __device__ inline Smem smem_layout(int nlim, int cap) {
   s.wB = take(sizeof(T) * (size_t)cap * R);
   s.toffA = take(sizeof(int32_t) * (ktm + 1));
   s.toffB = take(sizeof(int32_t) * (ktm + 1));
+  s.ordA = take(sizeof(int32_t) * (ktm + 1));
+  s.ordB = take(sizeof(int32_t) * (ktm + 1));
   s.zA = take(sizeof(int32_t) * (nlim + 1));
   s.zB = take(sizeof(int32_t) * (nlim + 1));
   s.uS = take(sizeof(T) * (nlim + 64));
@@ -222,8 +293,8 @@ __host__ __device__ inline Smem smem_layout(int nlim, int cap) {
 template <typename T, int KB, int NW, int R>
 __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dense, int32_t *lo_s,
                            double *fr_s, uint8_t *zflag, int32_t *zlist, int32_t *nz_out,
-                           int32_t *toff, int32_t *idx, T *wts, int cap, bool premul_rows,
-                           int32_t *misc) {
+                           int32_t *toff, int32_t *ord, int32_t *idx, T *wts, int cap,
+                           bool premul_rows, int32_t *misc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = NW * 32;
   const int n = G.n_nodes[g];
@@ -363,8 +434,33 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
       pos += __popc(bal);
     }
   }
+  // Tile schedule: tiles sorted by cost (entries) descending; phases hand
+  // them to warps in boustrophedon order (longest first), which balances the
+  // per-sweep work across warps for all ~70+ sweeps of this pair.
+  if (warp == 0) {
+    constexpr int SK = (32 * KB + R - 1) / R <= 32 ? 1 : ((32 * KB + R - 1) / R <= 64 ? 2 : 4);
+    int cv[SK], ci[SK];
+#pragma unroll
+    for (int c = 0; c < SK; c++) {
+      const int t = lane + 32 * c;
+      ci[c] = t;
+      cv[c] = (t < KT) ? (toff[t + 1] - toff[t] + 2) : -1;
+    }
+    warp_sort_desc<int, SK>(cv, ci, lane);
+#pragma unroll
+    for (int c = 0; c < SK; c++) {
+      const int q = lane + 32 * c;
+      if (q < KT) ord[q] = ci[c];
+    }
+  }
   __syncthreads();
   return true;
+}
+
+// q-th tile (0, 1, ...) of `warp` in the boustrophedon schedule; -1 when done.
+template <int NW>
+__device__ __forceinline__ int snake_slot(int m, int warp) {
+  return m * NW + ((m & 1) ? (NW - 1 - warp) : warp);
 }
 
 template <typename T, int KB, int NW, int R, int MINB>
@@ -372,7 +468,6 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     isorank_pair_kernel(DevCorpus CA, DevCorpus CB, PairWork work, PairOut out, PairParams prm,
                         unsigned long long *counter) {
   constexpr int NT = NW * 32;
-  constexpr int MAXT = ((32 * KB + R - 1) / R + NW - 1) / NW;  // column tiles per warp (phase B)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem L = smem_layout<T, R>(prm.nlim, prm.cap);
   T *Xs = (T *)(smem_raw + L.x);
@@ -384,6 +479,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   T *wB = (T *)(smem_raw + L.wB);
   int32_t *toffA = (int32_t *)(smem_raw + L.toffA);
   int32_t *toffB = (int32_t *)(smem_raw + L.toffB);
+  int32_t *ordA = (int32_t *)(smem_raw + L.ordA);
+  int32_t *ordB = (int32_t *)(smem_raw + L.ordB);
   int32_t *zA = (int32_t *)(smem_raw + L.zA);
   int32_t *zB = (int32_t *)(smem_raw + L.zB);
   T *uS = (T *)(smem_raw + L.uS);
@@ -424,6 +521,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         slot0 = 2 * (u - work.out_base);
         ndir = (a == b) ? 1 : 2;
       } else {
+        // one alignment per unordered pair, always in the caller's (lower
+        // index, higher index) direction — the reference's upper triangle —
+        // so results do not depend on the size-sorted schedule
+        if (ga > gb) { const int t = ga; ga = gb; gb = t; }
         slot0 = u - work.out_base;
       }
     }
@@ -443,10 +544,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       // ---- prologue: both operators (normalize_pair + _row_normalized)
       int32_t *nzA = misc + 1, *nzB = misc + 2;
       bool ok = build_side<T, KB, NW, R>(dir ? CB : CA, g1, N, P, dense, lo_s, fr_s, zflag, zA, nzA,
-                                         toffA, idxA, wA, prm.cap, true, misc);
+                                         toffA, ordA, idxA, wA, prm.cap, true, misc);
       if (ok)
-        ok = build_side<T, KB, NW, R>(C2, g2, N, P, dense, lo_s, fr_s, zflag, zB, nzB, toffB, idxB,
-                                      wB, prm.cap, false, misc);
+        ok = build_side<T, KB, NW, R>(C2, g2, N, P, dense, lo_s, fr_s, zflag, zB, nzB, toffB, ordB,
+                                      idxB, wB, prm.cap, false, misc);
       if (!ok) {
         if (tid == 0) {
           const int k = atomicAdd(out.ovf_count, 1);
@@ -466,17 +567,6 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         if (i < N && j < N) v = out.x0 ? (T)out.x0[(size_t)i * N + j] : (T)uni;
         Xs[e] = v;
       }
-      // owned elements (phase B mapping): rows k = lane + 32c, cols l = t*R + r
-      T xold[MAXT][KB][R];
-#pragma unroll
-      for (int m = 0; m < MAXT; m++)
-#pragma unroll
-        for (int c = 0; c < KB; c++)
-#pragma unroll
-          for (int r = 0; r < R; r++) {
-            const int k = lane + 32 * c, l = (warp + m * NW) * R + r;
-            xold[m][c][r] = (k < N && l < N) ? (out.x0 ? (T)out.x0[(size_t)k * N + l] : (T)uni) : (T)0;
-          }
       __syncthreads();
 
       const T teleport = (T)((1.0 - prm.alpha) * uni);  // (1-alpha)*uniform, :140
@@ -514,92 +604,96 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 
         // ---- phase A: Y[k, j] = sum_e wA[e][k-k0] X[i_e, j] + u[j]/N, j in [0, N]
         {
+          const bool extra = (N + 1 > 32 * KB);  // column N falls beyond the lane chunks
           T ucol[KB];
 #pragma unroll
           for (int c = 0; c < KB; c++) ucol[c] = uS[lane + 32 * c] * (T)invN;
-          for (int t = warp; t < KT; t += NW) {
-            T acc[KB][R];
+          const T ux = uS[N] * (T)invN;
+          for (int m = 0;; m++) {
+            const int q = snake_slot<NW>(m, warp);
+            if (q >= KT) break;
+            const int t = ordA[q];
+            // the rank-1 term u[j]/N seeds the accumulators
+            T acc[KB][R], accx[R];
 #pragma unroll
-            for (int c = 0; c < KB; c++)
+            for (int r = 0; r < R; r++) {
+              accx[r] = ux;
 #pragma unroll
-              for (int r = 0; r < R; r++) acc[c][r] = 0;
-            const int e1 = toffA[t + 1];
-#pragma unroll 2
-            for (int e = toffA[t]; e < e1; e++) {
-              const int ioff = idxA[e];
-              T w[R];
-              load_w<T, R>(wA + e * R, w);
-#pragma unroll
-              for (int c = 0; c < KB; c++) {
-                const T x = Xs[ioff + lane + 32 * c];
-#pragma unroll
-                for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], x, acc[c][r]);
-              }
+              for (int c = 0; c < KB; c++) acc[c][r] = ucol[c];
             }
+            if (extra)
+              tile_accumulate_rows<T, KB, R, true>(idxA, wA, Xs, toffA[t], toffA[t + 1], lane, N, acc, accx);
+            else
+              tile_accumulate_rows<T, KB, R, false>(idxA, wA, Xs, toffA[t], toffA[t + 1], lane, N, acc, accx);
 #pragma unroll
             for (int r = 0; r < R; r++) {
               const int k = t * R + r;
-              if (k < N) {
+              T *yrow = Ys + k * P;
 #pragma unroll
-                for (int c = 0; c < KB; c++) {
-                  const int j = lane + 32 * c;
-                  if (j <= N) Ys[k * P + j] = acc[c][r] + ucol[c];
-                }
+              for (int c = 0; c < KB; c++) {
+                const int j = lane + 32 * c;
+                if (k < N && j <= N) yrow[j] = acc[c][r];
               }
+              if (extra && lane == 0 && k < N) yrow[N] = accx[r];
             }
           }
         }
         __syncthreads();
 
-        // ---- phase B: F[k, l] for owned tiles; reductions
+        // ---- phase B: F[k, l] = alpha' (Y B')[k, l] + teleport; X_old is read
+        //      back from Xs (it holds the previous F, scale r_old) just before
+        //      the new F overwrites it.  Branch-free: padded lanes/columns are
+        //      computed on finite padding and masked out of the sums.
         const T alpha_eff = (T)(prm.alpha * r_old);
+        const T rold = (T)r_old;
         T sl = 0, dl = 0, ml = 0;
         {
-          T vrow[KB];
+          // lanes past row N-1 work on row N-1 (finite data) and are masked out
+          T vrow[KB], mk[KB];
+          int krow[KB];
 #pragma unroll
           for (int c = 0; c < KB; c++) {
             const int k = lane + 32 * c;
-            vrow[c] = (k < N) ? Ys[k * P + N] * (T)invN : (T)0;
+            krow[c] = (k < N ? k : N - 1) * P;
+            vrow[c] = Ys[krow[c] + N] * (T)invN;  // v[k]/N seeds the accumulators
+            mk[c] = (k < N) ? (T)1 : (T)0;
           }
-          const T rold = (T)r_old;
+          for (int m = 0;; m++) {
+            const int q = snake_slot<NW>(m, warp);
+            if (q >= KT) break;
+            const int t = ordB[q];
+            T acc[KB][R];
 #pragma unroll
-          for (int m = 0; m < MAXT; m++) {
-            const int t = warp + m * NW;
-            if (t < KT) {
-              T acc[KB][R];
+            for (int c = 0; c < KB; c++)
 #pragma unroll
-              for (int c = 0; c < KB; c++)
-#pragma unroll
-                for (int r = 0; r < R; r++) acc[c][r] = 0;
-              const int e1 = toffB[t + 1];
+              for (int r = 0; r < R; r++) acc[c][r] = vrow[c];
+            const int e1 = toffB[t + 1];
 #pragma unroll 2
-              for (int e = toffB[t]; e < e1; e++) {
-                const int j = idxB[e];
-                T w[R];
-                load_w<T, R>(wB + e * R, w);
-#pragma unroll
-                for (int c = 0; c < KB; c++) {
-                  const T y = Ys[(lane + 32 * c) * P + j];
-#pragma unroll
-                  for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], y, acc[c][r]);
-                }
-              }
+            for (int e = toffB[t]; e < e1; e++) {
+              const int j = idxB[e];
+              T w[R];
+              load_w<T, R>(wB + e * R, w);
 #pragma unroll
               for (int c = 0; c < KB; c++) {
-                const int k = lane + 32 * c;
+                const T y = Ys[krow[c] + j];
 #pragma unroll
-                for (int r = 0; r < R; r++) {
-                  const int l = t * R + r;
-                  if (k < N && l < N) {
-                    const T f = fma(alpha_eff, acc[c][r] + vrow[c], teleport);
-                    const T diff = fma(-xold[m][c][r], rold, f);
-                    sl += f;
-                    dl += fabs(diff);
-                    ml += copysign(f, diff);
-                    xold[m][c][r] = f;
-                    Xs[k * P + l] = f;
-                  }
-                }
+                for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], y, acc[c][r]);
+              }
+            }
+            const int lv = N - t * R;  // valid columns in this tile (>= 1)
+#pragma unroll
+            for (int c = 0; c < KB; c++) {
+              const int k = lane + 32 * c;
+              T *xrow = Xs + krow[c] + t * R;
+#pragma unroll
+              for (int r = 0; r < R; r++) {
+                const T msk = (r < lv) ? mk[c] : (T)0;
+                const T f = fma(alpha_eff, acc[c][r], teleport);
+                const T diff = fma(-xrow[r], rold, f);
+                sl = fma(msk, f, sl);
+                dl = fma(msk, fabs(diff), dl);
+                ml = fma(msk, copysign(f, diff), ml);
+                if (k < N && r < lv) xrow[r] = f;
               }
             }
           }
@@ -633,87 +727,89 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         }
       }
 
-      // ---- epilogue: normalised X into Xs, greedy matching (similarity.py:96-108)
+      // ---- epilogue: X = F * r (normalised) in place
       {
         const T rr = (T)r_old;
-#pragma unroll
-        for (int m = 0; m < MAXT; m++)
-#pragma unroll
-          for (int c = 0; c < KB; c++)
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-              const int k = lane + 32 * c, l = (warp + m * NW) * R + r;
-              if (k < N && l < N) Xs[k * P + l] = xold[m][c][r] * rr;
-            }
+        for (int e = tid; e < N * P; e += NT) {
+          const int i = e / P, j = e - (e / P) * P;
+          if (j < N) Xs[i * P + j] *= rr;
+        }
       }
       __syncthreads();
-      // row maxima (value desc, column asc), cached in Ys scratch
-      T *rmv = Ys;
-      int32_t *rmc = (int32_t *)(Ys + (N + 32));
-      int32_t *mS = rmc + (N + 32);
+      // Greedy matching, similarity.py:96-108.  Each row's columns are sorted
+      // once into the reference's order (value desc, column asc); a round then
+      // takes the best current head over active rows (ties -> lowest row,
+      // i.e. lowest row-major index overall) and advances only the rows whose
+      // head column was just taken.  Same matching as repeated global argmax.
+      uint8_t *ord = (uint8_t *)Ys;  // N x N column order (N <= 255)
+      int32_t *mS = (int32_t *)((uint8_t *)Ys + (((size_t)N * N + 15) & ~(size_t)15));
       for (int i = warp; i < N; i += NW) {
-        T bv = (T)-1;
-        int bc = 0x7fffffff;
+        T v[KB];
+        int c[KB];
 #pragma unroll
-        for (int c = 0; c < KB; c++) {
-          const int j = lane + 32 * c;
-          if (j < N) {
-            const T v = Xs[i * P + j];
-            if (v > bv) { bv = v; bc = j; }
-          }
+        for (int cc = 0; cc < KB; cc++) {
+          const int j = lane + 32 * cc;
+          v[cc] = (j < N) ? Xs[i * P + j] : (T)-1;
+          c[cc] = j;
         }
-        warp_argmax(bv, bc);
-        if (lane == 0) { rmv[i] = bv; rmc[i] = bc; }
+        warp_sort_desc<T, KB>(v, c, lane);
+#pragma unroll
+        for (int cc = 0; cc < KB; cc++) {
+          const int pos = lane + 32 * cc;
+          if (pos < N) ord[i * N + pos] = (uint8_t)c[cc];
+        }
       }
       __syncthreads();
       if (warp == 0) {
-        bool active[KB], taken[KB];
+        int ptr[KB], ccol[KB];
+        T cur[KB];
+        bool act[KB];
+        uint32_t taken[KB];
 #pragma unroll
-        for (int c = 0; c < KB; c++) {
-          active[c] = (lane + 32 * c) < N;
-          taken[c] = (lane + 32 * c) >= N;
+        for (int cc = 0; cc < KB; cc++) {
+          const int i = lane + 32 * cc;
+          act[cc] = i < N;
+          ptr[cc] = 0;
+          taken[cc] = 0u;
+          ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
+          cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
         }
         for (int round = 0; round < N; round++) {
           T bv = (T)-2;
           int brow = 0x7fffffff;
 #pragma unroll
-          for (int c = 0; c < KB; c++) {
-            const int i = lane + 32 * c;
-            if (active[c]) {
-              const T v = rmv[i];
-              if (v > bv || (v == bv && i < brow)) { bv = v; brow = i; }
-            }
-          }
+          for (int cc = 0; cc < KB; cc++)
+            if (act[cc] && cur[cc] > bv) { bv = cur[cc]; brow = lane + 32 * cc; }
           warp_argmax(bv, brow);
-          const int bcol = rmc[brow];
+          int mycol = 0;
+#pragma unroll
+          for (int cc = 0; cc < KB; cc++)
+            if (cc == (brow >> 5)) mycol = ccol[cc];
+          const int bcol = __shfl_sync(0xffffffffu, mycol, brow & 31);
           if (lane == 0) mS[brow] = bcol;
 #pragma unroll
-          for (int c = 0; c < KB; c++) {
-            if (lane + 32 * c == brow) active[c] = false;
-            if (lane + 32 * c == bcol) taken[c] = true;
+          for (int cc = 0; cc < KB; cc++) {
+            if (lane + 32 * cc == brow) act[cc] = false;
+            if (cc == (bcol >> 5)) taken[cc] |= 1u << (bcol & 31);
           }
-          __syncwarp();
-          // rows whose cached argmax column was just taken: recompute
 #pragma unroll
-          for (int c = 0; c < KB; c++) {
-            const int i = lane + 32 * c;
-            unsigned bal = __ballot_sync(0xffffffffu, active[c] && rmc[i] == bcol);
-            while (bal) {
-              const int q = __ffs(bal) - 1 + 32 * c;
-              bal &= bal - 1;
-              T qv = (T)-1;
-              int qc = 0x7fffffff;
+          for (int cc = 0; cc < KB; cc++) {
+            if (act[cc] && ccol[cc] == bcol) {
+              const int i = lane + 32 * cc;
+              int p = ptr[cc], col;
+              bool tk;
+              do {
+                ++p;
+                col = ord[i * N + p];
+                uint32_t word = 0;
 #pragma unroll
-              for (int c2 = 0; c2 < KB; c2++) {
-                const int j = lane + 32 * c2;
-                if (!taken[c2]) {
-                  const T v = Xs[q * P + j];
-                  if (v > qv) { qv = v; qc = j; }
-                }
-              }
-              warp_argmax(qv, qc);
-              if (lane == 0) { rmv[q] = qv; rmc[q] = qc; }
-              __syncwarp();
+                for (int q = 0; q < KB; q++)
+                  if (q == (col >> 5)) word = taken[q];
+                tk = (word >> (col & 31)) & 1u;
+              } while (tk);
+              ptr[cc] = p;
+              ccol[cc] = col;
+              cur[cc] = Xs[i * P + col];
             }
           }
         }

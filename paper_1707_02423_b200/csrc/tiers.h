@@ -1,0 +1,25 @@
+// Tier kernel instantiations live in tiers_f64.cu / tiers_f32.cu (compiled in
+// parallel); cfgsim.cu only takes their addresses.
+#pragma once
+#include "isorank.cuh"
+
+#define CFGSIM_TIER_LIST(X)      \
+  X(double, 1, 4, 4, 6)          \
+  X(double, 2, 8, 4, 3)          \
+  X(double, 4, 16, 4, 1)         \
+  X(float, 1, 4, 4, 6)           \
+  X(float, 2, 8, 4, 3)           \
+  X(float, 4, 16, 4, 1)
+
+#define CFGSIM_EXTERN_TIER(T, KB, NW, R, MINB)                                              \
+  extern template __global__ void cfgsim::isorank_pair_kernel<T, KB, NW, R, MINB>(         \
+      cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
+      cfgsim::PairParams, unsigned long long *);
+#define CFGSIM_INSTANTIATE_TIER(T, KB, NW, R, MINB)                                         \
+  template __global__ void cfgsim::isorank_pair_kernel<T, KB, NW, R, MINB>(                \
+      cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
+      cfgsim::PairParams, unsigned long long *);
+
+#ifndef CFGSIM_TIER_TU
+CFGSIM_TIER_LIST(CFGSIM_EXTERN_TIER)
+#endif
