@@ -22,6 +22,7 @@
 #include "../../include/cfgsim.h"
 #include "isorank.cuh"
 #include "tiers.h"
+#include "isorank_lr.cuh"
 
 using namespace cfgsim;
 
@@ -202,7 +203,7 @@ int cap_for(int precision, const Plan &pl, int nlim, bool dense) {
 }
 
 struct Scratch {
-  DBuf counters, ovf_count, ovf_list;
+  DBuf counters, ovf_count, ovf_list, gslab;
   int64_t ovf_cap = 0;
 };
 
@@ -217,7 +218,7 @@ Scratch &scratch_for(int device) {
 // Launch one tier over `work` (persistent grid, atomic work counter).
 int launch_tier(int precision, int ti, int nlim, int cap, const DevCorpus &A, const DevCorpus &B,
                 const PairWork &work, const PairOut &out, const cfgsim_params *p,
-                unsigned long long *counter, cudaStream_t st) {
+                unsigned long long *counter, cudaStream_t st, int force_m = 0) {
   const Tier &T = tiers(precision)[ti];
   const size_t smem = T.smem(nlim, cap);
   if (smem > kMaxSmem) return fail(CFGSIM_ERR_ARG, "tier shared memory exceeds 227 KB");
@@ -237,9 +238,110 @@ int launch_tier(int precision, int ti, int nlim, int cap, const DevCorpus &A, co
   prm.max_iter = p->max_iter;
   prm.cap = cap;
   prm.nlim = nlim;
+  static const int env_force_m = [] {  // CFGSIM_FORCE_M=1: exact delta every sweep (testing)
+    const char *e = getenv("CFGSIM_FORCE_M");
+    return (e && atoi(e) != 0) ? 1 : 0;
+  }();
+  prm.force_m = force_m | env_force_m;
   CU(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   void *args[] = {(void *)&A, (void *)&B, (void *)&work, (void *)&out, (void *)&prm, (void *)&counter};
   CU(cudaLaunchKernel(T.fn, dim3((unsigned)grid), dim3(T.nw * 32), args, smem, st));
+  g_launches++;
+  return CFGSIM_OK;
+}
+
+// ---------------------------------------------------------------- low-rank tiers
+// isorank_lowrank_kernel instantiations (isorank_lr.cuh): KB row chunks for
+// the prologue/epilogue, AR x BC entries per thread.  Launches are per exact
+// N, so the thread grid (TY x TX) and the vector padding fit N tightly.
+struct LRTier {
+  int nmax, kb, ar, bc;
+  const void *fn;
+};
+
+const std::vector<LRTier> &lr_tiers(int precision) {
+  static std::vector<LRTier> t64 = {
+      {32, 1, 4, 4, (const void *)isorank_lowrank_kernel<double, 1, 4, 4, 64, 10>},
+      {64, 2, 4, 8, (const void *)isorank_lowrank_kernel<double, 2, 4, 8, 128, 4>},
+      {128, 4, 4, 8, (const void *)isorank_lowrank_kernel<double, 4, 4, 8, 512, 1>}};
+  static std::vector<LRTier> t32 = {
+      {32, 1, 4, 4, (const void *)isorank_lowrank_kernel<float, 1, 4, 4, 64, 10>},
+      {64, 2, 4, 8, (const void *)isorank_lowrank_kernel<float, 2, 4, 8, 128, 5>},
+      {128, 4, 4, 8, (const void *)isorank_lowrank_kernel<float, 4, 4, 8, 512, 1>}};
+  return precision == CFGSIM_FP32 ? t32 : t64;
+}
+
+// CFGSIM_ALGO=dense selects the general two-product kernel for every pair
+// (A/B validation); default is the low-rank kernel whenever x0 is uniform.
+bool use_lowrank() {
+  static const bool lr = [] {
+    const char *e = getenv("CFGSIM_ALGO");
+    return !(e && std::string(e) == "dense");
+  }();
+  return lr;
+}
+
+bool lr_supported(int precision, int N) { return N <= lr_tiers(precision).back().nmax; }
+
+int lr_launch(int precision, int nlim, bool dense_lists, const DevCorpus &A, const DevCorpus &B,
+              const PairWork &work, const PairOut &out, const cfgsim_params *p, unsigned long long *counter,
+              cudaStream_t st) {
+  const auto &ts = lr_tiers(precision);
+  size_t ti = 0;
+  while (ti < ts.size() && nlim > ts[ti].nmax) ti++;
+  if (ti == ts.size()) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(nlim) + " exceeds the low-rank tiers");
+  const LRTier &T = ts[ti];
+  LRParams prm;
+  prm.alpha = p->alpha;
+  prm.tol = (precision == CFGSIM_FP32) ? std::max(p->tol, p->tol_fp32) : p->tol;
+  prm.max_iter = p->max_iter;
+  prm.nlim = nlim;
+  prm.ty = (nlim + T.ar - 1) / T.ar;
+  prm.tx = (nlim + T.bc - 1) / T.bc;
+  const int maxt = T.nmax <= 32 ? 64 : (T.nmax <= 64 ? 128 : 512);  // __launch_bounds__ of the tier
+  int nt = std::min(maxt, std::max(64, ((prm.ty * prm.tx + 31) / 32) * 32));
+  prm.np = (std::max(std::max(nlim, prm.ty * T.ar), prm.tx * T.bc) + 1) & ~1;
+  const int dc = nlim * nlim;
+  prm.cap = dense_lists ? dc : std::min(dc, 14 * nlim + 16);
+  // scratch placement: dense N x N operator/alignment in global memory for
+  // N > 64 (keeps several CTAs per SM); lists in global memory if they would
+  // not fit in shared memory (dense-bound reruns of large N)
+  const bool dglob = nlim > 64;
+  auto layout = [&](bool lg) {
+    return precision == CFGSIM_FP32 ? lr_smem_layout<float>(nlim, prm.cap, prm.np, dglob, lg)
+                                    : lr_smem_layout<double>(nlim, prm.cap, prm.np, dglob, lg);
+  };
+  bool lglob = false;
+  LRSmem L = layout(false);
+  if (L.total > kMaxSmem) {
+    if (!dglob) return fail(CFGSIM_ERR_ARG, "low-rank kernel shared memory exceeds 227 KB (N=" + std::to_string(nlim) + ")");
+    lglob = true;
+    L = layout(true);
+  }
+  prm.lists_global = lglob ? 1 : 0;
+  const size_t smem = L.total;
+  prm.gslab = nullptr;
+  prm.gslab_bytes = (int64_t)L.gtotal;
+  CU(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev, sms = 0, occ = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, T.fn, nt, smem));
+  if (occ < 1) return fail(CFGSIM_ERR_CUDA, "low-rank kernel cannot be resident (occupancy 0)");
+  int64_t grid = std::min<int64_t>((int64_t)sms * occ, work.n_items);
+  if (grid < 1) return CFGSIM_OK;
+  if (dglob) {
+    Scratch &S = scratch_for(dev);
+    const size_t need = (size_t)grid * L.gtotal;
+    if (S.gslab.n < need) {
+      CU(cudaStreamSynchronize(st));  // a previous launch may still use the old slab
+      CU(S.gslab.alloc(need));
+    }
+    prm.gslab = S.gslab.as<unsigned char>();
+  }
+  CU(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  void *args[] = {(void *)&A, (void *)&B, (void *)&work, (void *)&out, (void *)&prm, (void *)&counter};
+  CU(cudaLaunchKernel(T.fn, dim3((unsigned)grid), dim3(nt), args, smem, st));
   g_launches++;
   return CFGSIM_OK;
 }
@@ -300,7 +402,7 @@ struct OutStage {
 int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<int32_t> &ia,
              const std::vector<int32_t> &ib, const std::vector<int64_t> &slot, const cfgsim_params *p,
              double *d, double *W, int32_t *iters, uint8_t *conv, double *X, int32_t *match,
-             const double *x0, cudaStream_t st, int cap_mode = 0);
+             const double *x0, cudaStream_t st, int mode = 0);  // mode: 1 dense lists, 2 force_m
 
 int handle_overflow(const cfgsim_corpus *A, const cfgsim_corpus *B, const PairWork &work,
                     const cfgsim_params *p, double *d, double *W, int32_t *iters, uint8_t *conv,
@@ -312,27 +414,30 @@ int handle_overflow(const cfgsim_corpus *A, const cfgsim_corpus *B, const PairWo
   if (cnt > S.ovf_cap) return fail(CFGSIM_ERR_CUDA, "overflow list capacity exceeded");
   std::vector<int64_t> recs(cnt);
   CU(cudaMemcpy(recs.data(), S.ovf_list.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> ia, ib;
-  std::vector<int64_t> sl;
+  // kind 0: list overflow -> dense-bound lists; kind 1: ambiguous stop -> force_m
+  std::vector<int32_t> ia[2], ib[2];
+  std::vector<int64_t> sl[2];
   for (int64_t rec : recs) {
-    const int64_t item = rec >> 1;
-    const int dir = (int)(rec & 1);
-    if (work.mode == WORK_LIST) {
-      // caller's list arrays are on the device; we kept host copies in work.* (see run_list)
+    const int kind = (int)(rec & 1);
+    const int dir = (int)((rec >> 1) & 1);
+    if (work.mode == WORK_LIST)
       return fail(CFGSIM_ERR_CUDA, "internal: list overflow must be handled by run_list");
-    }
-    const int64_t u = work.u0 + item;
+    const int64_t u = rec >> 2;  // absolute unit
     const auto &rs = A->row_start;
     const int a = (int)(std::upper_bound(rs.begin(), rs.end(), u) - rs.begin()) - 1;
     const int b = a + (int)(u - rs[a]);
     int g1 = A->perm[a], g2 = A->perm[b];
     if (work.ordered ? dir != 0 : g1 > g2) std::swap(g1, g2);
-    ia.push_back(g1);
-    ib.push_back(g2);
-    sl.push_back(work.ordered ? 2 * (u - work.out_base) + dir : (u - work.out_base));
+    ia[kind].push_back(g1);
+    ib[kind].push_back(g2);
+    sl[kind].push_back(work.ordered ? 2 * (u - work.out_base) + dir : (u - work.out_base));
   }
   CU(cudaMemsetAsync(S.ovf_count.p, 0, sizeof(int32_t), st));
-  return run_list(A, B, ia, ib, sl, p, d, W, iters, conv, nullptr, nullptr, nullptr, st, 1);
+  for (int kind = 0; kind < 2; kind++)
+    if (int rc = run_list(A, B, ia[kind], ib[kind], sl[kind], p, d, W, iters, conv, nullptr, nullptr,
+                          nullptr, st, kind == 0 ? 1 : 2))
+      return rc;
+  return CFGSIM_OK;
 }
 
 int ensure_scratch(Scratch &S, int64_t ovf_cap) {
@@ -351,17 +456,28 @@ int ensure_scratch(Scratch &S, int64_t ovf_cap) {
 int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<int32_t> &ia,
              const std::vector<int32_t> &ib, const std::vector<int64_t> &slot, const cfgsim_params *p,
              double *d, double *W, int32_t *iters, uint8_t *conv, double *X, int32_t *match,
-             const double *x0, cudaStream_t st, int cap_mode) {
+             const double *x0, cudaStream_t st, int mode) {
+  const bool dense_lists = (mode & 1) != 0;
   const int64_t n = (int64_t)ia.size();
   if (n == 0) return CFGSIM_OK;
   Scratch &S = scratch_for(A->device);
   if (int rc = ensure_scratch(S, 1 << 16)) return rc;
-  // bucket by launch plan (tier, occupancy), within a bucket by descending N
+  // bucket by launch plan: low-rank kernel -> one launch per exact N;
+  // general kernel -> per (tier, occupancy), within a bucket by descending N
+  const bool lr = (x0 == nullptr) && use_lowrank();
   std::vector<Plan> plans;
   std::vector<std::vector<int64_t>> bucket;
   for (int64_t q = 0; q < n; q++) {
     const int N = std::max(A->n_nodes[ia[q]], B->n_nodes[ib[q]]);
-    const Plan pl = plan_for(p->precision, N, cap_mode != 0);
+    Plan pl;
+    if (lr) {
+      if (!lr_supported(p->precision, N))
+        return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds the on-chip tiers of this build");
+      pl.ti = N;  // bucket key
+      pl.occ = 0;
+    } else {
+      pl = plan_for(p->precision, N, dense_lists);
+    }
     if (pl.ti < 0)
       return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
                                       " exceeds the on-chip tiers of this build");
@@ -413,29 +529,38 @@ int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<i
     o.ovf_count = S.ovf_count.as<int32_t>();
     o.ovf_list = S.ovf_list.as<int64_t>();
     o.ovf_cap = (int32_t)S.ovf_cap;
-    const int cap2 = cap_for(p->precision, plans[bi], nlim, cap_mode != 0);
-    if (int rc = launch_tier(p->precision, ti, nlim, cap2, A->dev(), B->dev(), w, o, p,
+    if (lr) {
+      if (int rc = lr_launch(p->precision, nlim, dense_lists, A->dev(), B->dev(), w, o, p,
                              S.counters.as<unsigned long long>() + (bi % 32), st))
-      return rc;
-    // overflowed items: rerun with dense-bound lists
+        return rc;
+    } else {
+      const int cap2 = cap_for(p->precision, plans[bi], nlim, dense_lists);
+      if (int rc = launch_tier(p->precision, ti, nlim, cap2, A->dev(), B->dev(), w, o, p,
+                               S.counters.as<unsigned long long>() + (bi % 32), st, (mode & 2) ? 1 : 0))
+        return rc;
+    }
+    // overflowed / ambiguous items are re-run (dense-bound lists / force_m)
     int32_t cnt = 0;
     CU(cudaMemcpyAsync(&cnt, S.ovf_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (cnt > 0) {
-      if (cap_mode) return fail(CFGSIM_ERR_CUDA, "internal: dense-bound lists overflowed");
       if (cnt > S.ovf_cap) return fail(CFGSIM_ERR_CUDA, "overflow list capacity exceeded");
       std::vector<int64_t> recs(cnt);
       CU(cudaMemcpy(recs.data(), S.ovf_list.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
       CU(cudaMemset(S.ovf_count.p, 0, sizeof(int32_t)));
-      std::vector<int32_t> ra, rb;
-      std::vector<int64_t> rs;
+      std::vector<int32_t> ra[2], rb[2];
+      std::vector<int64_t> rs[2];
       for (int64_t rec : recs) {
-        const int64_t item = rec >> 1;
-        ra.push_back(hia[item]);
-        rb.push_back(hib[item]);
-        rs.push_back(hsl[item]);
+        const int kind = (int)(rec & 1);
+        const int64_t item = rec >> 2;
+        ra[kind].push_back(hia[item]);
+        rb[kind].push_back(hib[item]);
+        rs[kind].push_back(hsl[item]);
       }
-      if (int rc = run_list(A, B, ra, rb, rs, p, d, W, iters, conv, X, match, x0, st, 1)) return rc;
+      if (!ra[0].empty() && dense_lists) return fail(CFGSIM_ERR_CUDA, "internal: dense-bound lists overflowed");
+      if (!ra[1].empty() && (mode & 2)) return fail(CFGSIM_ERR_CUDA, "internal: ambiguous stop with force_m");
+      if (int rc = run_list(A, B, ra[0], rb[0], rs[0], p, d, W, iters, conv, X, match, x0, st, mode | 1)) return rc;
+      if (int rc = run_list(A, B, ra[1], rb[1], rs[1], p, d, W, iters, conv, X, match, x0, st, mode | 2)) return rc;
     }
   }
   return CFGSIM_OK;
@@ -709,51 +834,59 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Scratch &S = scratch_for(c->device);
   if (int rc = ensure_scratch(S, 1 << 16)) return rc;
-  const int nt = (int)tiers(p->precision).size();
-  // rows of the sorted corpus with N in a tier are contiguous: split the unit
-  // range at tier boundaries (n_sorted is descending).
+  const bool lr = use_lowrank();
+  // rows of the size-sorted corpus are contiguous per N: split the unit range
+  // into runs of rows with one launch plan (low-rank: one N per launch).
   int a = (int)(std::upper_bound(c->row_start.begin(), c->row_start.end(), u0) -
                 c->row_start.begin()) - 1;
   int64_t u = u0;
   int launch_no = 0;
+  PairWork w{};
+  w.mode = WORK_TRIANGLE;
+  w.ordered = ordered;
+  w.out_base = u0;
+  w.row_start = c->d_row_start.as<int64_t>();
+  w.perm = c->d_perm.as<int32_t>();
+  w.K = c->K;
+  PairOut o{};
+  o.d = d_lin;
+  o.iters = iters_lin;
+  o.ovf_count = S.ovf_count.as<int32_t>();
+  o.ovf_list = S.ovf_list.as<int64_t>();
+  o.ovf_cap = (int32_t)S.ovf_cap;
   while (u < u1) {
     const int N = c->n_sorted[a];
-    const Plan pl = plan_for(p->precision, N, false);
-    if (pl.ti < 0)
-      return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
-                                      " exceeds the on-chip tiers of this build");
-    // extend over rows with the same launch plan (rows are sorted by n desc)
     int a_end = a;
-    while (a_end + 1 < c->K && plan_for(p->precision, c->n_sorted[a_end + 1], false).same_launch(pl))
-      a_end++;
-    const int ti = pl.ti;
-    const int cap = cap_for(p->precision, pl, N, false);
+    Plan pl;
+    if (lr) {
+      if (!lr_supported(p->precision, N))
+        return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds the on-chip tiers of this build");
+      while (a_end + 1 < c->K && c->n_sorted[a_end + 1] == N) a_end++;
+    } else {
+      pl = plan_for(p->precision, N, false);
+      if (pl.ti < 0)
+        return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) +
+                                        " exceeds the on-chip tiers of this build");
+      while (a_end + 1 < c->K && plan_for(p->precision, c->n_sorted[a_end + 1], false).same_launch(pl))
+        a_end++;
+    }
     const int64_t seg_end = std::min(u1, c->row_start[a_end + 1]);
-    PairWork w{};
-    w.mode = WORK_TRIANGLE;
-    w.ordered = ordered;
     w.n_items = seg_end - u;
     w.u0 = u;
-    w.out_base = u0;
-    w.row_start = c->d_row_start.as<int64_t>();
-    w.perm = c->d_perm.as<int32_t>();
-    w.K = c->K;
-    PairOut o{};
-    o.d = d_lin;
-    o.iters = iters_lin;
-    o.ovf_count = S.ovf_count.as<int32_t>();
-    o.ovf_list = S.ovf_list.as<int64_t>();
-    o.ovf_cap = (int32_t)S.ovf_cap;
-    if (launch_no >= 60) return fail(CFGSIM_ERR_CUDA, "too many tier segments");
-    if (int rc = launch_tier(p->precision, ti, N, cap, c->dev(), c->dev(), w, o, p,
-                             S.counters.as<unsigned long long>() + launch_no, st))
-      return rc;
+    unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no % 64);
+    if (lr) {
+      if (int rc = lr_launch(p->precision, N, false, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
+    } else {
+      if (int rc = launch_tier(p->precision, pl.ti, N, cap_for(p->precision, pl, N, false), c->dev(), c->dev(),
+                               w, o, p, ctr, st))
+        return rc;
+    }
     launch_no++;
-    if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
     u = seg_end;
     a = a_end + 1;
-    (void)nt;
   }
+  // overflowed / ambiguous pairs of all runs (records hold absolute units)
+  if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
   CU(cudaGetLastError());
   return CFGSIM_OK;
 }

@@ -79,8 +79,9 @@ struct PairParams {
   double alpha;
   double tol;
   int32_t max_iter;
-  int32_t cap;   // list entries per side
-  int32_t nlim;  // max N this launch is sized for
+  int32_t cap;      // list entries per side
+  int32_t nlim;     // max N this launch is sized for
+  int32_t force_m;  // accumulate the delta correction term every sweep
 };
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
@@ -140,6 +141,34 @@ __device__ inline double np_pairwise_sum(const double *a, int n) {
     }
   }
   return ret;
+}
+
+// np_pairwise_sum computed by a warp, bit-identical: for 8 <= n <= 128 the
+// eight strided partial sums r[k] = a[k] + a[k+8] + ... run on lanes 0..7 in
+// numpy's order, then lane 0 combines them with numpy's fixed tree and adds
+// the tail; other n use the serial routine on lane 0.  Result on all lanes.
+__device__ inline double warp_pairwise_sum(const double *a, int n, int lane) {
+  double res = 0.0;
+  if (n >= 8 && n <= 128) {
+    const int full = n - (n % 8);
+    double r = 0.0;
+    if (lane < 8) {
+      r = a[lane];
+      for (int i = 8 + lane; i < full; i += 8) r = __dadd_rn(r, a[i]);
+    }
+    const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+    const double p01 = __dadd_rn(r, r1);          // lanes 0,2,4,6: r[k] + r[k+1]
+    const double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+    const double q = __dadd_rn(p01, p23);         // lanes 0,4: (r0+r1)+(r2+r3), (r4+r5)+(r6+r7)
+    const double q4 = __shfl_down_sync(0xffffffffu, q, 4);
+    if (lane == 0) {
+      res = __dadd_rn(q, q4);
+      for (int i = full; i < n; i++) res = __dadd_rn(res, a[i]);
+    }
+  } else if (lane == 0) {
+    res = np_pairwise_sum(a, n);
+  }
+  return __shfl_sync(0xffffffffu, res, 0);
 }
 
 // R consecutive weights as one or two 16-byte shared loads (broadcast).
@@ -223,6 +252,38 @@ __device__ __forceinline__ void warp_sort_desc(T (&v)[KB], int (&c)[KB], int lan
   }
 }
 
+// Warp-wide bitonic sort of 32*KB distinct unsigned keys, descending.
+template <int KB>
+__device__ __forceinline__ void warp_sort_keys_desc(unsigned long long (&v)[KB], int lane) {
+  constexpr int n = 32 * KB;
+#pragma unroll
+  for (int k = 2; k <= n; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int cc = 0; cc < KB; cc++) {
+          const int pc = cc ^ (j >> 5);
+          if (pc > cc) {
+            const bool up = ((cc * 32 + lane) & k) == 0;
+            const bool sw = up ? (v[pc] > v[cc]) : (v[cc] > v[pc]);
+            if (sw) { const unsigned long long t = v[cc]; v[cc] = v[pc]; v[pc] = t; }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < KB; cc++) {
+          const unsigned long long ov = __shfl_xor_sync(0xffffffffu, v[cc], j);
+          const bool lower = (lane & j) == 0;
+          const bool up = ((cc * 32 + lane) & k) == 0;
+          const unsigned long long hi = ov > v[cc] ? ov : v[cc], lo = ov > v[cc] ? v[cc] : ov;
+          v[cc] = (lower == up) ? hi : lo;
+        }
+      }
+    }
+  }
+}
+
 // Phase A inner loop over one tile's entries: acc[c][r] += w_e[r] * X[i_e, lane+32c];
 // EXTRA also accumulates column xcol (= N when N == 32*KB) uniformly.
 template <typename T, int KB, int R, bool EXTRA>
@@ -290,13 +351,14 @@ __host__ __device__ inline Smem smem_layout(int nlim, int cap) {
 // Build the row-normalised operator of one side (similarity.py:85-93 after
 // matrix.py:74-106) into the dense fp64 scratch `dense` (N x N, pitch N),
 // then extract its column-tile lists.  Returns false on list overflow.
-template <typename T, int KB, int NW, int R>
+// `dense` needs N * (N|1) doubles (shared or global memory).
+template <typename T, int KB, int R, bool SORT_TILES>
 __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dense, int32_t *lo_s,
                            double *fr_s, uint8_t *zflag, int32_t *zlist, int32_t *nz_out,
                            int32_t *toff, int32_t *ord, int32_t *idx, T *wts, int cap,
                            bool premul_rows, int32_t *misc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NT = NW * 32;
+  const int NT = blockDim.x, NW = NT >> 5;
   const int n = G.n_nodes[g];
   const int32_t *rp = G.rowptr + G.rp_off[g];
   const int32_t *cc = G.col + G.nz_off[g];
@@ -314,9 +376,11 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
     __syncthreads();
   }
 
-  // Rows of A-hat, one warp per target row.
+  // Rows of A-hat, one warp per target row (scratch pitch DP = N|1: odd, so
+  // the column scans below are bank-conflict free).
+  const int DP = N | 1;
   for (int p = warp; p < N; p += NW) {
-    double *row = dense + (size_t)p * N;
+    double *row = dense + (size_t)p * DP;
     if (n == N) {
       for (int q = lane; q < N; q += 32) row[q] = 0.0;
       __syncwarp();
@@ -349,12 +413,11 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
       }
     }
     __syncwarp();
-    double s = 0.0;
-    if (lane == 0) s = np_pairwise_sum(row, N);  // similarity.py:89
-    s = shfl_d(s, 0);
+    const double s = warp_pairwise_sum(row, N, lane);  // similarity.py:89
     if (lane == 0) zflag[p] = (s == 0.0);
     if (s != 0.0)
-      for (int q = lane; q < N; q += 32) row[q] = __ddiv_rn(row[q], s);  // :92
+      for (int q = lane; q < N; q += 32)
+        if (row[q] != 0.0) row[q] = __ddiv_rn(row[q], s);  // :92 (0/s == 0)
   }
   __syncthreads();
 
@@ -382,7 +445,7 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
 #pragma unroll
         for (int r = 0; r < R; r++) {
           const int k = t * R + r;
-          if (k < N && dense[(size_t)i * N + k] != 0.0) nzr = true;
+          if (k < N && dense[(size_t)i * DP + k] != 0.0) nzr = true;
         }
       }
       cnt += __popc(__ballot_sync(0xffffffffu, nzr));
@@ -420,7 +483,7 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
 #pragma unroll
       for (int r = 0; r < R; r++) {
         const int k = t * R + r;
-        w[r] = (i < N && k < N) ? dense[(size_t)i * N + k] : 0.0;
+        w[r] = (i < N && k < N) ? dense[(size_t)i * DP + k] : 0.0;
         if (w[r] != 0.0) nzr = true;
       }
       if (i >= N || zflag[i]) nzr = false;
@@ -437,7 +500,7 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
   // Tile schedule: tiles sorted by cost (entries) descending; phases hand
   // them to warps in boustrophedon order (longest first), which balances the
   // per-sweep work across warps for all ~70+ sweeps of this pair.
-  if (warp == 0) {
+  if (SORT_TILES && warp == 0) {
     constexpr int SK = (32 * KB + R - 1) / R <= 32 ? 1 : ((32 * KB + R - 1) / R <= 64 ? 2 : 4);
     int cv[SK], ci[SK];
 #pragma unroll
@@ -461,6 +524,288 @@ __device__ bool build_side(const DevCorpus &G, int g, int N, int P, double *dens
 template <int NW>
 __device__ __forceinline__ int snake_slot(int m, int warp) {
   return m * NW + ((m & 1) ? (NW - 1 - warp) : warp);
+}
+
+// d from the matched weight, similarity.py:160-173
+__device__ __forceinline__ double isorank_distance_of(double w, int N) {
+  if (N == 1) return 1.0;
+  double cn = (w - 1.0 / N) / (1.0 - 1.0 / N);
+  cn = fmin(1.0, fmax(0.0, cn));
+  return 1.0 + (1.0 - cn);
+}
+
+// Greedy matching, similarity.py:96-108, on X (N x N, pitch P, in shared
+// memory).  Each row's columns are sorted once into the reference's order
+// (value desc, column asc); a round then takes the best current head over
+// active rows (ties -> lowest row, i.e. lowest row-major index overall) and
+// advances only the rows whose head column was just taken — the same
+// matching as repeated global argmax.  `scr` needs N*N + 4N + 32 bytes.
+// Call with the whole CTA; returns W = sum_i X[i, match(i)] (similarity.py:150)
+// to every thread.
+template <typename T, int KB>
+__device__ double greedy_match(const T *Xs, int P, int N, uint8_t *scr, int lane, int warp, int NW,
+                               int32_t *match_out) {
+  uint8_t *ord = scr;  // N x N column order (N <= 255)
+  int32_t *mS = (int32_t *)(scr + (((size_t)N * N + 15) & ~(size_t)15));
+  double *wres = (double *)(mS + ((N + 3) & ~3));
+  // column bits and the exponent span a packed key can hold
+  constexpr int CB = (32 * KB <= 64) ? 6 : ((32 * KB <= 128) ? 7 : 8);
+  constexpr int EB = (sizeof(T) == 8) ? 12 - CB : 8;  // exponent bits left in 64
+  for (int i = warp; i < N; i += NW) {
+    T v[KB];
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int j = lane + 32 * cc;
+      v[cc] = (j < N) ? Xs[i * P + j] : (T)0;
+    }
+    // X > 0 (teleport floor): if the row's exponent span fits in EB bits,
+    // (value desc, column asc) is one unsigned key: rebased exponent |
+    // mantissa | (mask - column), sorted as integers (exact, no fp compare).
+    int emin = 0x7fffffff, emax = -1;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++)
+      if (lane + 32 * cc < N) {
+        const int e = (sizeof(T) == 8) ? (int)((__double_as_longlong((double)v[cc]) >> 52) & 0x7ff)
+                                       : (int)((__float_as_uint((float)v[cc]) >> 23) & 0xff);
+        emin = min(emin, e);
+        emax = max(emax, e);
+      }
+    emin = __reduce_min_sync(0xffffffffu, emin);
+    emax = __reduce_max_sync(0xffffffffu, emax);
+    if (emin > 0 && emax - emin < (1 << EB)) {
+      unsigned long long key[KB];  // padding lanes (j >= N) keep 0 and sort last:
+                                   // real keys have a column field >= 1 then
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++) {
+        const int j = lane + 32 * cc;
+        unsigned long long k = 0ull;  // padding sorts last
+        if (j < N) {
+          if (sizeof(T) == 8) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong((double)v[cc]);
+            const unsigned long long e = ((b >> 52) & 0x7ff) - (unsigned long long)emin;
+            const unsigned long long m = b & ((1ull << 52) - 1);
+            k = (e << (52 + CB)) | (m << CB) | (unsigned long long)((1 << CB) - 1 - j);
+          } else {
+            const unsigned int b = __float_as_uint((float)v[cc]);
+            const unsigned long long e = ((b >> 23) & 0xff) - (unsigned)emin;
+            k = (e << (23 + CB)) | ((unsigned long long)(b & 0x7fffff) << CB) |
+                (unsigned long long)((1 << CB) - 1 - j);
+          }
+        }
+        key[cc] = k;
+      }
+      warp_sort_keys_desc<KB>(key, lane);
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++) {
+        const int pos = lane + 32 * cc;
+        if (pos < N) ord[i * N + pos] = (uint8_t)((1 << CB) - 1 - (int)(key[cc] & ((1ull << CB) - 1)));
+      }
+    } else {
+      int c[KB];
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++) {
+        const int j = lane + 32 * cc;
+        c[cc] = j;
+        if (j >= N) v[cc] = (T)-1;
+      }
+      warp_sort_desc<T, KB>(v, c, lane);
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++) {
+        const int pos = lane + 32 * cc;
+        if (pos < N) ord[i * N + pos] = (uint8_t)c[cc];
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int ptr[KB], ccol[KB];
+    T cur[KB];
+    bool act[KB];
+    uint32_t taken[KB];
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int i = lane + 32 * cc;
+      act[cc] = i < N;
+      ptr[cc] = 0;
+      taken[cc] = 0u;
+      ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
+      cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
+    }
+    for (int round = 0; round < N; round++) {
+      T bv = (T)0;
+      int brow = 0x7fffffff;
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++)
+        if (act[cc] && (brow == 0x7fffffff || cur[cc] > bv)) { bv = cur[cc]; brow = lane + 32 * cc; }
+      // warp argmax (value desc, row asc) with integer reductions: X > 0, so
+      // the IEEE bit pattern orders like the value
+      if (sizeof(T) == 8) {
+        const unsigned long long b = (brow == 0x7fffffff) ? 0ull : (unsigned long long)__double_as_longlong((double)bv);
+        const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        brow = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)brow : 0x7fffffffu);
+      } else {
+        const unsigned b = (brow == 0x7fffffff) ? 0u : __float_as_uint((float)bv);
+        const unsigned mb = __reduce_max_sync(0xffffffffu, b);
+        brow = (int)__reduce_min_sync(0xffffffffu, b == mb ? (unsigned)brow : 0x7fffffffu);
+      }
+      int mycol = 0;
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++)
+        if (cc == (brow >> 5)) mycol = ccol[cc];
+      const int bcol = __shfl_sync(0xffffffffu, mycol, brow & 31);
+      if (lane == 0) mS[brow] = bcol;
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++) {
+        if (lane + 32 * cc == brow) act[cc] = false;
+        if (cc == (bcol >> 5)) taken[cc] |= 1u << (bcol & 31);
+      }
+#pragma unroll
+      for (int cc = 0; cc < KB; cc++) {
+        if (act[cc] && ccol[cc] == bcol) {
+          const int i = lane + 32 * cc;
+          int p = ptr[cc], col;
+          bool tk;
+          do {
+            ++p;
+            col = ord[i * N + p];
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < KB; q++)
+              if (q == (col >> 5)) word = taken[q];
+            tk = (word >> (col & 31)) & 1u;
+          } while (tk);
+          ptr[cc] = p;
+          ccol[cc] = col;
+          cur[cc] = Xs[i * P + col];
+        }
+      }
+    }
+    __syncwarp();
+    double wsum = 0.0;  // fixed-order tree
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int i = lane + 32 * cc;
+      if (i < N) wsum += (double)Xs[i * P + mS[i]];
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, m);
+    if (lane == 0) *wres = wsum;
+    if (match_out)
+      for (int i = lane; i < N; i += 32) match_out[i] = mS[i];
+  }
+  __syncthreads();
+  return *wres;
+}
+
+// Phase A of one sweep for this warp: Y[k, j] = u[j]/N + sum_e w_e[k] X[i_e, j]
+// over its tiles (output rows k = t*R .. t*R+R-1), lanes over columns j.
+template <typename T, int KB, int NW, int R>
+__device__ __forceinline__ void phase_a(const T *__restrict__ Xs, T *__restrict__ Ys, const int32_t *__restrict__ idxA,
+                                        const T *__restrict__ wA, const int32_t *__restrict__ toffA,
+                                        const int32_t *__restrict__ ordA, const int32_t *__restrict__ zA, int nzA,
+                                        int N, int P, int KT, T invN, int lane, int warp) {
+  T ucol[KB];  // u[j] / N, computed by every warp from the uniform rows of A'
+#pragma unroll
+  for (int c = 0; c < KB; c++) ucol[c] = 0;
+  for (int e = 0; e < nzA; e++) {
+    const int zo = zA[e] * P + lane;
+#pragma unroll
+    for (int c = 0; c < KB; c++) ucol[c] += Xs[zo + 32 * c];
+  }
+#pragma unroll
+  for (int c = 0; c < KB; c++) ucol[c] *= invN;
+  for (int m = 0;; m++) {
+    const int q = snake_slot<NW>(m, warp);
+    if (q >= KT) break;
+    const int t = ordA[q];
+    T acc[KB][R], accx[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      accx[r] = 0;
+#pragma unroll
+      for (int c = 0; c < KB; c++) acc[c][r] = ucol[c];
+    }
+    tile_accumulate_rows<T, KB, R, false>(idxA, wA, Xs, toffA[t], toffA[t + 1], lane, N, acc, accx);
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int k = t * R + r;
+      T *yrow = Ys + k * P;
+#pragma unroll
+      for (int c = 0; c < KB; c++) {
+        const int j = lane + 32 * c;
+        if (k < N && j < N) yrow[j] = acc[c][r];
+      }
+    }
+  }
+}
+
+// Phase B of one sweep for this warp: F[k, l] = alpha' (v[k]/N + sum_e w_e[l]
+// Y[k, j_e]) + teleport over its tiles (columns l), lanes over rows k.  X_old
+// is re-read from Xs just before F overwrites it.  Branch-free: padded lanes
+// and columns run on finite data and are masked out of the sums.
+template <typename T, int KB, int NW, int R, bool NEEDM>
+__device__ __forceinline__ void phase_b(T *__restrict__ Xs, const T *__restrict__ Ys, const int32_t *__restrict__ idxB,
+                                        const T *__restrict__ wB, const int32_t *__restrict__ toffB,
+                                        const int32_t *__restrict__ ordB, const int32_t *__restrict__ zB, int nzB,
+                                        int N, int P, int KT, T invN, T alpha_eff, T rold, T teleport, int lane,
+                                        int warp, T &sl, T &dl, T &ml) {
+  T vrow[KB], mk[KB];
+  int krow[KB];
+#pragma unroll
+  for (int c = 0; c < KB; c++) {
+    const int k = lane + 32 * c;
+    krow[c] = (k < N ? k : N - 1) * P;
+    mk[c] = (k < N) ? (T)1 : (T)0;
+    vrow[c] = 0;
+  }
+  for (int e = 0; e < nzB; e++) {
+    const int zj = zB[e];
+#pragma unroll
+    for (int c = 0; c < KB; c++) vrow[c] += Ys[krow[c] + zj];
+  }
+#pragma unroll
+  for (int c = 0; c < KB; c++) vrow[c] *= invN;
+  for (int m = 0;; m++) {
+    const int q = snake_slot<NW>(m, warp);
+    if (q >= KT) break;
+    const int t = ordB[q];
+    T acc[KB][R];
+#pragma unroll
+    for (int c = 0; c < KB; c++)
+#pragma unroll
+      for (int r = 0; r < R; r++) acc[c][r] = vrow[c];
+    const int e1 = toffB[t + 1];
+#pragma unroll 2
+    for (int e = toffB[t]; e < e1; e++) {
+      const int j = idxB[e];
+      T w[R];
+      load_w<T, R>(wB + e * R, w);
+#pragma unroll
+      for (int c = 0; c < KB; c++) {
+        const T y = Ys[krow[c] + j];
+#pragma unroll
+        for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], y, acc[c][r]);
+      }
+    }
+    const int lv = N - t * R;  // valid columns in this tile (>= 1)
+#pragma unroll
+    for (int c = 0; c < KB; c++) {
+      const int k = lane + 32 * c;
+      T *xrow = Xs + krow[c] + t * R;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const T msk = (r < lv) ? mk[c] : (T)0;
+        const T f = fma(alpha_eff, acc[c][r], teleport);
+        const T diff = fma(-xrow[r], rold, f);
+        sl = fma(msk, f, sl);
+        dl = fma(msk, fabs(diff), dl);
+        if (NEEDM) ml = fma(msk, copysign(f, diff), ml);
+        if (k < N && r < lv) xrow[r] = f;
+      }
+    }
+  }
 }
 
 template <typename T, int KB, int NW, int R, int MINB>
@@ -543,15 +888,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 
       // ---- prologue: both operators (normalize_pair + _row_normalized)
       int32_t *nzA = misc + 1, *nzB = misc + 2;
-      bool ok = build_side<T, KB, NW, R>(dir ? CB : CA, g1, N, P, dense, lo_s, fr_s, zflag, zA, nzA,
+      bool ok = build_side<T, KB, R, true>(dir ? CB : CA, g1, N, P, dense, lo_s, fr_s, zflag, zA, nzA,
                                          toffA, ordA, idxA, wA, prm.cap, true, misc);
       if (ok)
-        ok = build_side<T, KB, NW, R>(C2, g2, N, P, dense, lo_s, fr_s, zflag, zB, nzB, toffB, ordB,
+        ok = build_side<T, KB, R, true>(C2, g2, N, P, dense, lo_s, fr_s, zflag, zB, nzB, toffB, ordB,
                                       idxB, wB, prm.cap, false, misc);
       if (!ok) {
         if (tid == 0) {
           const int k = atomicAdd(out.ovf_count, 1);
-          if (k < out.ovf_cap) out.ovf_list[k] = item * 2 + dir;
+          if (k < out.ovf_cap) out.ovf_list[k] = ((work.mode == WORK_TRIANGLE ? work.u0 + item : item) << 2) | (dir << 1);
           if (out.iters) out.iters[slot] = -1;
         }
         __syncthreads();
@@ -570,134 +915,28 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       __syncthreads();
 
       const T teleport = (T)((1.0 - prm.alpha) * uni);  // (1-alpha)*uniform, :140
-      double r_old = 1.0;
+      double r_old = 1.0, dp_prev = 1e300;
       int it_done = prm.max_iter;
-      bool converged = false;
+      bool converged = false, ambiguous = false;
 
       for (int it = 1; it <= prm.max_iter; it++) {
-        // ---- phase U: u = z_A^T X (columns 0..N-1), g = X z_B (column N),
-        //      u[N] = z_A^T X z_B
-        for (int q = tid; q < 2 * N; q += NT) {
-          if (q < N) {
-            T su = 0;
-            for (int e = 0; e < nzAv; e++) su += Xs[zA[e] * P + q];
-            uS[q] = su;
-          } else {
-            const int i = q - N;
-            T sg = 0;
-            for (int e = 0; e < nzBv; e++) sg += Xs[i * P + zB[e]];
-            Xs[i * P + N] = sg;
-          }
-        }
-        if (warp == NW - 1) {
-          T s = 0;
-          const int tot = nzAv * nzBv;
-          for (int q = lane; q < tot; q += 32) {
-            const int e = q / nzBv, f = q - (q / nzBv) * nzBv;
-            s += Xs[zA[e] * P + zB[f]];
-          }
-#pragma unroll
-          for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-          if (lane == 0) uS[N] = s;
-        }
+        // ---- phase A: Y = A'^T X = S_A^T X + 1 u^T / N   (u = z_A^T X)
+        phase_a<T, KB, NW, R>(Xs, Ys, idxA, wA, toffA, ordA, zA, nzAv, N, P, KT, (T)invN, lane, warp);
         __syncthreads();
 
-        // ---- phase A: Y[k, j] = sum_e wA[e][k-k0] X[i_e, j] + u[j]/N, j in [0, N]
-        {
-          const bool extra = (N + 1 > 32 * KB);  // column N falls beyond the lane chunks
-          T ucol[KB];
-#pragma unroll
-          for (int c = 0; c < KB; c++) ucol[c] = uS[lane + 32 * c] * (T)invN;
-          const T ux = uS[N] * (T)invN;
-          for (int m = 0;; m++) {
-            const int q = snake_slot<NW>(m, warp);
-            if (q >= KT) break;
-            const int t = ordA[q];
-            // the rank-1 term u[j]/N seeds the accumulators
-            T acc[KB][R], accx[R];
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-              accx[r] = ux;
-#pragma unroll
-              for (int c = 0; c < KB; c++) acc[c][r] = ucol[c];
-            }
-            if (extra)
-              tile_accumulate_rows<T, KB, R, true>(idxA, wA, Xs, toffA[t], toffA[t + 1], lane, N, acc, accx);
-            else
-              tile_accumulate_rows<T, KB, R, false>(idxA, wA, Xs, toffA[t], toffA[t + 1], lane, N, acc, accx);
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-              const int k = t * R + r;
-              T *yrow = Ys + k * P;
-#pragma unroll
-              for (int c = 0; c < KB; c++) {
-                const int j = lane + 32 * c;
-                if (k < N && j <= N) yrow[j] = acc[c][r];
-              }
-              if (extra && lane == 0 && k < N) yrow[N] = accx[r];
-            }
-          }
-        }
-        __syncthreads();
-
-        // ---- phase B: F[k, l] = alpha' (Y B')[k, l] + teleport; X_old is read
-        //      back from Xs (it holds the previous F, scale r_old) just before
-        //      the new F overwrites it.  Branch-free: padded lanes/columns are
-        //      computed on finite padding and masked out of the sums.
-        const T alpha_eff = (T)(prm.alpha * r_old);
-        const T rold = (T)r_old;
+        // ---- phase B: F = alpha' (Y S_B + v 1^T / N) + teleport  (v = Y z_B);
+        //      m (first-order normalisation correction of delta) is only
+        //      accumulated once delta is within 64x of tol.
+        const bool need_m = prm.force_m || (dp_prev < 64.0 * prm.tol);
         T sl = 0, dl = 0, ml = 0;
-        {
-          // lanes past row N-1 work on row N-1 (finite data) and are masked out
-          T vrow[KB], mk[KB];
-          int krow[KB];
-#pragma unroll
-          for (int c = 0; c < KB; c++) {
-            const int k = lane + 32 * c;
-            krow[c] = (k < N ? k : N - 1) * P;
-            vrow[c] = Ys[krow[c] + N] * (T)invN;  // v[k]/N seeds the accumulators
-            mk[c] = (k < N) ? (T)1 : (T)0;
-          }
-          for (int m = 0;; m++) {
-            const int q = snake_slot<NW>(m, warp);
-            if (q >= KT) break;
-            const int t = ordB[q];
-            T acc[KB][R];
-#pragma unroll
-            for (int c = 0; c < KB; c++)
-#pragma unroll
-              for (int r = 0; r < R; r++) acc[c][r] = vrow[c];
-            const int e1 = toffB[t + 1];
-#pragma unroll 2
-            for (int e = toffB[t]; e < e1; e++) {
-              const int j = idxB[e];
-              T w[R];
-              load_w<T, R>(wB + e * R, w);
-#pragma unroll
-              for (int c = 0; c < KB; c++) {
-                const T y = Ys[krow[c] + j];
-#pragma unroll
-                for (int r = 0; r < R; r++) acc[c][r] = fma(w[r], y, acc[c][r]);
-              }
-            }
-            const int lv = N - t * R;  // valid columns in this tile (>= 1)
-#pragma unroll
-            for (int c = 0; c < KB; c++) {
-              const int k = lane + 32 * c;
-              T *xrow = Xs + krow[c] + t * R;
-#pragma unroll
-              for (int r = 0; r < R; r++) {
-                const T msk = (r < lv) ? mk[c] : (T)0;
-                const T f = fma(alpha_eff, acc[c][r], teleport);
-                const T diff = fma(-xrow[r], rold, f);
-                sl = fma(msk, f, sl);
-                dl = fma(msk, fabs(diff), dl);
-                ml = fma(msk, copysign(f, diff), ml);
-                if (k < N && r < lv) xrow[r] = f;
-              }
-            }
-          }
-        }
+        const T alpha_eff = (T)(prm.alpha * r_old);
+        if (need_m)
+          phase_b<T, KB, NW, R, true>(Xs, Ys, idxB, wB, toffB, ordB, zB, nzBv, N, P, KT, (T)invN, alpha_eff,
+                                      (T)r_old, teleport, lane, warp, sl, dl, ml);
+        else
+          phase_b<T, KB, NW, R, false>(Xs, Ys, idxB, wB, toffB, ordB, zB, nzBv, N, P, KT, (T)invN, alpha_eff,
+                                       (T)r_old, teleport, lane, warp, sl, dl, ml);
+
         // block reduction in a fixed order (deterministic, no atomics)
         double s3[3] = {(double)sl, (double)dl, (double)ml};
 #pragma unroll
@@ -710,21 +949,39 @@ __global__ void __launch_bounds__(NW * 32, MINB)
           red[warp * 3 + 2] = s3[2];
         }
         __syncthreads();
-        double s = 0, dp = 0, mm = 0;
+        // every lane sums the NW partials with the same butterfly: identical
+        // results in all warps
+        const int src = lane % NW;
+        double s = red[src * 3 + 0], dp = red[src * 3 + 1], mm = red[src * 3 + 2];
 #pragma unroll
-        for (int w = 0; w < NW; w++) {
-          s += red[w * 3 + 0];
-          dp += red[w * 3 + 1];
-          mm += red[w * 3 + 2];
+        for (int m = NW / 2; m > 0; m >>= 1) {
+          s += shfl_xor_d(s, m);
+          dp += shfl_xor_d(dp, m);
+          mm += shfl_xor_d(mm, m);
         }
         const double r = 1.0 / s;  // fresh /= fresh.sum(), :141
-        const double delta = dp + (r - 1.0) * mm;  // sum |fresh - x|, :142
+        // sum |fresh - x| (:142) = dp + (r - 1) m to first order in |1 - s|
+        const double delta = need_m ? dp + (r - 1.0) * mm : dp;
+        if (!need_m && fabs(dp - prm.tol) <= 1.01 * fabs(1.0 - s) + 1e-300) {
+          ambiguous = true;  // cannot decide without m: re-run this pair with force_m
+          break;
+        }
         r_old = r;
+        dp_prev = dp;
         if (delta < prm.tol) {  // :144
           it_done = it;
           converged = true;
           break;
         }
+      }
+      if (ambiguous) {
+        if (tid == 0) {
+          const int k = atomicAdd(out.ovf_count, 1);
+          if (k < out.ovf_cap) out.ovf_list[k] = ((work.mode == WORK_TRIANGLE ? work.u0 + item : item) << 2) | (dir << 1) | 1;
+          if (out.iters) out.iters[slot] = -2;
+        }
+        __syncthreads();
+        continue;
       }
 
       // ---- epilogue: X = F * r (normalised) in place
@@ -736,109 +993,14 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         }
       }
       __syncthreads();
-      // Greedy matching, similarity.py:96-108.  Each row's columns are sorted
-      // once into the reference's order (value desc, column asc); a round then
-      // takes the best current head over active rows (ties -> lowest row,
-      // i.e. lowest row-major index overall) and advances only the rows whose
-      // head column was just taken.  Same matching as repeated global argmax.
-      uint8_t *ord = (uint8_t *)Ys;  // N x N column order (N <= 255)
-      int32_t *mS = (int32_t *)((uint8_t *)Ys + (((size_t)N * N + 15) & ~(size_t)15));
-      for (int i = warp; i < N; i += NW) {
-        T v[KB];
-        int c[KB];
-#pragma unroll
-        for (int cc = 0; cc < KB; cc++) {
-          const int j = lane + 32 * cc;
-          v[cc] = (j < N) ? Xs[i * P + j] : (T)-1;
-          c[cc] = j;
-        }
-        warp_sort_desc<T, KB>(v, c, lane);
-#pragma unroll
-        for (int cc = 0; cc < KB; cc++) {
-          const int pos = lane + 32 * cc;
-          if (pos < N) ord[i * N + pos] = (uint8_t)c[cc];
-        }
-      }
-      __syncthreads();
-      if (warp == 0) {
-        int ptr[KB], ccol[KB];
-        T cur[KB];
-        bool act[KB];
-        uint32_t taken[KB];
-#pragma unroll
-        for (int cc = 0; cc < KB; cc++) {
-          const int i = lane + 32 * cc;
-          act[cc] = i < N;
-          ptr[cc] = 0;
-          taken[cc] = 0u;
-          ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
-          cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
-        }
-        for (int round = 0; round < N; round++) {
-          T bv = (T)-2;
-          int brow = 0x7fffffff;
-#pragma unroll
-          for (int cc = 0; cc < KB; cc++)
-            if (act[cc] && cur[cc] > bv) { bv = cur[cc]; brow = lane + 32 * cc; }
-          warp_argmax(bv, brow);
-          int mycol = 0;
-#pragma unroll
-          for (int cc = 0; cc < KB; cc++)
-            if (cc == (brow >> 5)) mycol = ccol[cc];
-          const int bcol = __shfl_sync(0xffffffffu, mycol, brow & 31);
-          if (lane == 0) mS[brow] = bcol;
-#pragma unroll
-          for (int cc = 0; cc < KB; cc++) {
-            if (lane + 32 * cc == brow) act[cc] = false;
-            if (cc == (bcol >> 5)) taken[cc] |= 1u << (bcol & 31);
-          }
-#pragma unroll
-          for (int cc = 0; cc < KB; cc++) {
-            if (act[cc] && ccol[cc] == bcol) {
-              const int i = lane + 32 * cc;
-              int p = ptr[cc], col;
-              bool tk;
-              do {
-                ++p;
-                col = ord[i * N + p];
-                uint32_t word = 0;
-#pragma unroll
-                for (int q = 0; q < KB; q++)
-                  if (q == (col >> 5)) word = taken[q];
-                tk = (word >> (col & 31)) & 1u;
-              } while (tk);
-              ptr[cc] = p;
-              ccol[cc] = col;
-              cur[cc] = Xs[i * P + col];
-            }
-          }
-        }
-        __syncwarp();
-        // W = sum_i X[i, match(i)] (similarity.py:150), fixed-order tree
-        double wsum = 0.0;
-#pragma unroll
-        for (int c = 0; c < KB; c++) {
-          const int i = lane + 32 * c;
-          if (i < N) wsum += (double)Xs[i * P + mS[i]];
-        }
-#pragma unroll
-        for (int m = 16; m > 0; m >>= 1) wsum += shfl_xor_d(wsum, m);
-        if (lane == 0) {
-          double dist;  // similarity.py:160-173
-          if (N == 1) {
-            dist = 1.0;
-          } else {
-            double cn = (wsum - 1.0 / N) / (1.0 - 1.0 / N);
-            cn = fmin(1.0, fmax(0.0, cn));
-            dist = 1.0 + (1.0 - cn);
-          }
-          if (out.d) out.d[slot] = dist;
+      {
+        const double wsum = greedy_match<T, KB>(Xs, P, N, (uint8_t *)Ys, lane, warp, NT >> 5, out.match);
+        if (tid == 0) {
+          if (out.d) out.d[slot] = isorank_distance_of(wsum, N);
           if (out.W) out.W[slot] = wsum;
           if (out.iters) out.iters[slot] = it_done;
           if (out.conv) out.conv[slot] = converged ? 1 : 0;
         }
-        if (out.match)
-          for (int i = lane; i < N; i += 32) out.match[i] = mS[i];
       }
       if (out.X)
         for (int e = tid; e < N * N; e += NT) out.X[e] = (double)Xs[(e / N) * P + (e % N)];

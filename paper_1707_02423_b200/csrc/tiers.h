@@ -2,6 +2,7 @@
 // parallel); cfgsim.cu only takes their addresses.
 #pragma once
 #include "isorank.cuh"
+#include "isorank_lr.cuh"
 
 #define CFGSIM_TIER_LIST(X)      \
   X(double, 1, 4, 4, 6)          \
@@ -20,6 +21,23 @@
       cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
       cfgsim::PairParams, unsigned long long *);
 
+#define CFGSIM_EXTERN_LR(T, KB, AR, BC, MAXT, MINB)                                                     \
+  extern template __global__ void cfgsim::isorank_lowrank_kernel<T, KB, AR, BC, MAXT, MINB>(           \
+      cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
+      cfgsim::LRParams, unsigned long long *);
+#define CFGSIM_INSTANTIATE_LR(T, KB, AR, BC, MAXT, MINB)                                                \
+  template __global__ void cfgsim::isorank_lowrank_kernel<T, KB, AR, BC, MAXT, MINB>(                  \
+      cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
+      cfgsim::LRParams, unsigned long long *);
+#define CFGSIM_LR_LIST(X) \
+  X(double, 1, 4, 4, 64, 10)  \
+  X(double, 2, 4, 8, 128, 4)  \
+  X(double, 4, 4, 8, 512, 1)  \
+  X(float, 1, 4, 4, 64, 10)   \
+  X(float, 2, 4, 8, 128, 5)   \
+  X(float, 4, 4, 8, 512, 1)
+
 #ifndef CFGSIM_TIER_TU
 CFGSIM_TIER_LIST(CFGSIM_EXTERN_TIER)
+CFGSIM_LR_LIST(CFGSIM_EXTERN_LR)
 #endif

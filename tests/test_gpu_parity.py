@@ -254,3 +254,47 @@ def test_degenerate_graphs(P):
         d = P.measure_distance(mat(P, a), mat(P, b), P.MeasureId.ISO)
         r = ffi.iso_pair(a, b)
         assert d == pytest.approx(r["d"], rel=RTOL64)
+
+
+def test_lazy_delta_correction_is_exact(P, c2_sample):
+    """The normalisation correction term of delta is only accumulated near
+    convergence; forcing it every sweep must not change any result."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_1707_02423_b200 as P; from paper_1707_02423_b200 import synth;"
+            "m = synth.random_corpus(40, 16, 64, seed=5);"
+            "t = [P.TransitionMatrix(f'g{i:03d}', x, tuple(range(len(x))), P.ROW_STOCHASTIC) for i, x in enumerate(m)];"
+            "pm, it = P.pairwise(t, P.MeasureId.ISO, return_iterations=True);"
+            "np.save(sys.argv[1], np.concatenate([pm.scores.ravel(), it.ravel().astype(float)]))")
+    outs = []
+    for force in ("0", "1"):
+        path = f"/tmp/cfgsim_force_m_{force}.npy"
+        env = dict(os.environ, CFGSIM_FORCE_M=force)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, cwd=str(GOLDEN.parent.parent))
+        outs.append(np.load(path))
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_lowrank_and_two_product_kernels_agree(P):
+    """The default (closed-form, rank-structured) kernel and the general
+    two-product kernel (CFGSIM_ALGO=dense) compute the same iterates."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_1707_02423_b200 as P; from paper_1707_02423_b200 import synth;"
+            "m = synth.random_corpus(60, 16, 100, seed=21);"
+            "t = [P.TransitionMatrix(f'g{i:03d}', x, tuple(range(len(x))), P.ROW_STOCHASTIC) for i, x in enumerate(m)];"
+            "pm, it = P.pairwise(t, P.MeasureId.ISO, return_iterations=True, symmetric=False);"
+            "np.save(sys.argv[1], np.concatenate([pm.scores.ravel(), it.ravel().astype(float)]))")
+    outs = []
+    for algo in ("lowrank", "dense"):
+        path = f"/tmp/cfgsim_algo_{algo}.npy"
+        env = dict(os.environ, CFGSIM_ALGO=algo)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, cwd=str(GOLDEN.parent.parent))
+        outs.append(np.load(path))
+    n = len(outs[0]) // 2
+    np.testing.assert_array_equal(outs[0][n:], outs[1][n:])  # iteration counts
+    np.testing.assert_allclose(outs[0][:n], outs[1][:n], rtol=1e-12)
