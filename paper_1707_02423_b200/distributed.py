@@ -1,0 +1,114 @@
+"""All-pairs ISO across GPUs: cost-balanced triangle ranges + one all-gather.
+
+SURVEY §8(e): pairs are independent, so each rank aligns a contiguous range
+of units of the size-sorted upper triangle (no collective while aligning);
+the only exchange is one ``all_gather_into_tensor`` of the per-rank score
+tiles (NCCL over NVLink on GPUs, gloo in the CPU tests), after which every
+rank scatters the unit vector into the K x K matrix.  Per-pair arithmetic
+does not depend on the schedule, so results are bitwise identical for any
+world size.
+
+The unit enumeration and the split mirror ``cfgsim_allpairs_split`` /
+``cfgsim_allpairs_scatter`` in ``csrc/cfgsim.cu`` (checked against each other
+in the GPU tests).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+from .workload import triangle_units
+
+
+def row_starts(k: int) -> np.ndarray:
+    return np.concatenate([[0], np.cumsum(np.arange(k, 0, -1))]).astype(np.int64)
+
+
+def split_units(n_nodes: np.ndarray, world: int) -> np.ndarray:
+    """world+1 unit boundaries balancing sum N^2 per rank (N = n of the row's
+    graph; rows sorted by n descending, stable)."""
+    n_nodes = np.asarray(n_nodes)
+    k = len(n_nodes)
+    ns = n_nodes[np.argsort(-n_nodes, kind="stable")].astype(np.float64)
+    rs = row_starts(k)
+    per_row = (k - np.arange(k)) * ns * ns
+    cum = np.concatenate([[0.0], np.cumsum(per_row)])
+    total = cum[-1]
+    bounds = np.zeros(world + 1, np.int64)
+    for r in range(1, world):
+        target = total * r / world
+        a = int(np.searchsorted(cum, target, side="right")) - 1
+        a_c = min(a, k - 1)
+        per = ns[a_c] * ns[a_c]
+        u = rs[a] + int(np.ceil((target - cum[a]) / per))
+        u = min(u, rs[min(a + 1, k)])
+        bounds[r] = max(u, bounds[r - 1])
+    bounds[world] = rs[k]
+    return bounds
+
+
+def scatter_units(n_nodes: np.ndarray, d_units: np.ndarray) -> np.ndarray:
+    """Unit-linear (unordered, symmetric) scores -> K x K matrix, caller's order."""
+    perm, a, b = triangle_units(n_nodes)
+    k = len(n_nodes)
+    out = np.empty((k, k))
+    out[perm[a], perm[b]] = d_units
+    out[perm[b], perm[a]] = d_units
+    return out
+
+
+def unit_pairs(n_nodes: np.ndarray, u0: int, u1: int) -> tuple[np.ndarray, np.ndarray]:
+    """Graph indices (low id, high id) of units [u0, u1) — the direction the
+    kernels align in."""
+    perm, a, b = triangle_units(n_nodes)
+    ga, gb = perm[a[u0:u1]], perm[b[u0:u1]]
+    return np.minimum(ga, gb), np.maximum(ga, gb)
+
+
+def allpairs_sharded(n_nodes: np.ndarray, compute_range: Callable[[int, int], np.ndarray], *, group=None,
+                     device=None):
+    """Run ``compute_range(u0, u1) -> d[u1-u0]`` on this rank's share and
+    all-gather; returns the K x K matrix on every rank.
+
+    ``compute_range`` is the GPU kernel call in production
+    (``DeviceCorpus`` + ``cfgsim_allpairs_range``) and the CPU oracle in the
+    gloo tests."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    bounds = split_units(n_nodes, world)
+    u0, u1 = int(bounds[rank]), int(bounds[rank + 1])
+    chunk = int(max(bounds[1:] - bounds[:-1]))
+    local = np.zeros(chunk)
+    local[: u1 - u0] = compute_range(u0, u1)
+    dev = device if device is not None else torch.device("cpu")
+    t_local = torch.as_tensor(local, dtype=torch.float64, device=dev)
+    if world > 1:
+        gathered = torch.empty(world * chunk, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(gathered, t_local, group=group)
+        g = gathered.cpu().numpy()
+        full = np.concatenate([g[r * chunk: r * chunk + int(bounds[r + 1] - bounds[r])] for r in range(world)])
+    else:
+        full = local[: u1 - u0]
+    return scatter_units(n_nodes, full)
+
+
+def gpu_compute_range(corpus, params, stream=None):
+    """compute_range backed by the sm_100a kernels (device-resident corpus)."""
+    import torch
+
+    from . import _native as nat
+
+    def run(u0: int, u1: int) -> np.ndarray:
+        out = torch.empty(max(u1 - u0, 1), dtype=torch.float64, device=torch.device("cuda", corpus.device))
+        if u1 > u0:
+            nat.check(nat.lib.cfgsim_allpairs_range(corpus.handle, u0, u1, 0, nat.C.byref(params), nat.ptr(out),
+                                                    None, stream))
+        torch.cuda.synchronize(corpus.device)
+        return out[: u1 - u0].cpu().numpy()
+
+    return run
