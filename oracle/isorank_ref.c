@@ -131,6 +131,24 @@ int oracle_iso_pair(int na, const double *A, int nb, const double *B, double alp
   row_normalize(ap, N); /* similarity.py:133 */
   row_normalize(bp, N);
 
+  /* nonzero lists of B' rows (for the second product) */
+  long *bnz_ptr = (long *)malloc(sizeof(long) * (N + 1));
+  long nnzb = 0;
+  for (long e = 0; e < NN; e++) nnzb += bp[e] != 0.0;
+  int *bnz_col = (int *)malloc(sizeof(int) * (nnzb + 1));
+  double *bnz_val = (double *)malloc(sizeof(double) * (nnzb + 1));
+  if (!bnz_ptr || !bnz_col || !bnz_val) return 2;
+  nnzb = 0;
+  for (int j = 0; j < N; j++) {
+    bnz_ptr[j] = nnzb;
+    for (int l = 0; l < N; l++)
+      if (bp[(long)j * N + l] != 0.0) {
+        bnz_col[nnzb] = l;
+        bnz_val[nnzb++] = bp[(long)j * N + l];
+      }
+  }
+  bnz_ptr[N] = nnzb;
+
   const double uniform = 1.0 / (double)NN; /* :134 */
   if (x0) {
     memcpy(x, x0, sizeof(double) * NN); /* caller passes start/sum(start) (:135) */
@@ -150,15 +168,14 @@ int oracle_iso_pair(int na, const double *A, int nb, const double *B, double alp
         double *yk = y + (long)k * N;
         for (int j = 0; j < N; j++) yk[j] += a * xi[j];
       }
-    /* z = y B' : z[k,l] += y[k,j] * B'[j,l] */
+    /* z = y B' : z[k,l] += y[k,j] * B'[j,l] (j ascending; zero entries of B'
+     * skipped via its nonzero lists, which leaves every sum unchanged) */
     memset(z, 0, sizeof(double) * NN);
     for (int k = 0; k < N; k++)
       for (int j = 0; j < N; j++) {
         const double yv = y[(long)k * N + j];
-        const double *bj = bp + (long)j * N;
         double *zk = z + (long)k * N;
-        for (int l = 0; l < N; l++)
-          if (bj[l] != 0.0) zk[l] += yv * bj[l];
+        for (long e = bnz_ptr[j]; e < bnz_ptr[j + 1]; e++) zk[bnz_col[e]] += yv * bnz_val[e];
       }
     /* :140  fresh = alpha*kx + (1-alpha)*uniform */
     const double teleport = (1.0 - alpha) * uniform;
@@ -195,6 +212,9 @@ int oracle_iso_pair(int na, const double *A, int nb, const double *B, double alp
   if (W_out) *W_out = w;
   if (iters_out) *iters_out = it;
   if (conv_out) *conv_out = (uint8_t)conv;
+  free(bnz_ptr);
+  free(bnz_col);
+  free(bnz_val);
   free(ap);
   free(bp);
   free(x);

@@ -84,6 +84,7 @@ struct cfgsim_corpus {
   std::vector<int32_t> n_sorted;  // n of perm[a]
   std::vector<int64_t> row_start; // triangle units: K+1
   DBuf d_n, d_rp_off, d_rowptr, d_nz_off, d_col, d_val, d_perm, d_row_start;
+  DBuf d_cscp, d_csc_row, d_csc_val;  // transposed copy (large-N kernel)
   int64_t bytes = 0;
   DevCorpus dev() const {
     DevCorpus c;
@@ -94,6 +95,9 @@ struct cfgsim_corpus {
     c.nz_off = d_nz_off.as<int64_t>();
     c.col = d_col.as<int32_t>();
     c.val = d_val.as<double>();
+    c.cscp = d_cscp.as<int32_t>();
+    c.csc_row = d_csc_row.as<int32_t>();
+    c.csc_val = d_csc_val.as<double>();
     return c;
   }
 };
@@ -203,7 +207,7 @@ int cap_for(int precision, const Plan &pl, int nlim, bool dense) {
 }
 
 struct Scratch {
-  DBuf counters, ovf_count, ovf_list, gslab;
+  DBuf counters, ovf_count, ovf_list, gslab, status;
   int64_t ovf_cap = 0;
 };
 
@@ -346,6 +350,90 @@ int lr_launch(int precision, int nlim, bool dense_lists, const DevCorpus &A, con
   return CFGSIM_OK;
 }
 
+// ---------------------------------------------------------------- large-N kernel
+// isorank_big_kernel (isorank_big.cuh) for 128 < N <= 1024: one launch per
+// sort class (N <= 32 KB), slab per CTA sized for the launch's largest N.
+constexpr int kBigNmax = 1024;
+constexpr int kBigKey = 1 << 20;  // bucket keys above any N
+
+int big_kb(int N) { return N <= 256 ? 8 : (N <= 512 ? 16 : 32); }
+
+const void *big_fn(int precision, int kb) {
+  if (precision == CFGSIM_FP32)
+    return kb == 8 ? (const void *)isorank_big_kernel<float, 8>
+                   : (kb == 16 ? (const void *)isorank_big_kernel<float, 16> : (const void *)isorank_big_kernel<float, 32>);
+  return kb == 8 ? (const void *)isorank_big_kernel<double, 8>
+                 : (kb == 16 ? (const void *)isorank_big_kernel<double, 16> : (const void *)isorank_big_kernel<double, 32>);
+}
+
+// Iterations after which the delta bracket (isorank_big.cuh) certainly stops:
+// delta_k <= 4 alpha^k (1 + eps).
+int big_kcap(double alpha, double tol, int max_iter) {
+  double a = 1.0;
+  for (int k = 1; k <= max_iter; k++) {
+    a *= alpha;
+    if (4.01 * a < tol) return std::min(max_iter, k + 1);
+  }
+  return max_iter;
+}
+
+int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, const PairWork &work,
+               const PairOut &out, const cfgsim_params *p, unsigned long long *counter, cudaStream_t st) {
+  if (nlim > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(nlim) + " exceeds 1024");
+  const int kb = big_kb(nlim);
+  const void *fn = big_fn(precision, kb);
+  BigParams prm;
+  prm.alpha = p->alpha;
+  prm.tol = (precision == CFGSIM_FP32) ? std::max(p->tol, p->tol_fp32) : p->tol;
+  prm.eps = (precision == CFGSIM_FP32) ? 0.02 : 1e-6;
+  prm.max_iter = p->max_iter;
+  prm.kcap = big_kcap(p->alpha, prm.tol, p->max_iter);
+  prm.nlim = nlim;
+  const size_t smem = precision == CFGSIM_FP32 ? big_smem_layout<float>(nlim).total : big_smem_layout<double>(nlim).total;
+  const size_t slab = precision == CFGSIM_FP32 ? big_slab_layout<float>(nlim, prm.kcap).total
+                                               : big_slab_layout<double>(nlim, prm.kcap).total;
+  if (smem > kMaxSmem) return fail(CFGSIM_ERR_ARG, "large-N kernel shared memory exceeds 227 KB");
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev, sms = 0, occ = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BIG_THREADS, smem));
+  if (occ < 1) return fail(CFGSIM_ERR_CUDA, "large-N kernel cannot be resident (occupancy 0)");
+  const int64_t grid = std::min<int64_t>((int64_t)sms * occ, work.n_items);
+  if (grid < 1) return CFGSIM_OK;
+  Scratch &S = scratch_for(dev);
+  const size_t need = (size_t)grid * slab;
+  if (S.gslab.n < need) {
+    CU(cudaStreamSynchronize(st));  // a previous launch may still use the old slab
+    CU(S.gslab.alloc(need));
+  }
+  if (!S.status.p) {
+    CU(S.status.alloc(sizeof(int32_t)));
+    CU(cudaMemset(S.status.p, 0, sizeof(int32_t)));
+  }
+  prm.slab = S.gslab.as<unsigned char>();
+  prm.slab_bytes = (int64_t)slab;
+  prm.status = S.status.as<int32_t>();
+  CU(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  void *args[] = {(void *)&A, (void *)&B, (void *)&work, (void *)&out, (void *)&prm, (void *)&counter};
+  CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(BIG_THREADS), args, smem, st));
+  g_launches++;
+  return CFGSIM_OK;
+}
+
+// internal-error flag of the large-N kernel (synchronises the stream)
+int big_status(Scratch &S, cudaStream_t st) {
+  if (!S.status.p) return CFGSIM_OK;
+  int32_t v = 0;
+  CU(cudaMemcpyAsync(&v, S.status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (v) {
+    CU(cudaMemset(S.status.p, 0, sizeof(int32_t)));
+    return fail(CFGSIM_ERR_CUDA, "internal: large-N kernel iteration history overflow");
+  }
+  return CFGSIM_OK;
+}
+
 int check_params(const cfgsim_params *p) {
   if (!p) return fail(CFGSIM_ERR_ARG, "params is NULL");
   if (!(p->alpha > 0.0 && p->alpha < 1.0))
@@ -471,9 +559,13 @@ int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<i
     const int N = std::max(A->n_nodes[ia[q]], B->n_nodes[ib[q]]);
     Plan pl;
     if (lr) {
-      if (!lr_supported(p->precision, N))
-        return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds the on-chip tiers of this build");
-      pl.ti = N;  // bucket key
+      if (lr_supported(p->precision, N)) {
+        pl.ti = N;  // bucket key: one low-rank launch per exact N
+      } else if (N <= kBigNmax) {
+        pl.ti = kBigKey + big_kb(N);  // large-N kernel, one launch per sort class
+      } else {
+        return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
+      }
       pl.occ = 0;
     } else {
       pl = plan_for(p->precision, N, dense_lists);
@@ -529,7 +621,12 @@ int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<i
     o.ovf_count = S.ovf_count.as<int32_t>();
     o.ovf_list = S.ovf_list.as<int64_t>();
     o.ovf_cap = (int32_t)S.ovf_cap;
-    if (lr) {
+    if (lr && ti >= kBigKey) {
+      if (int rc = big_launch(p->precision, nlim, A->dev(), B->dev(), w, o, p,
+                              S.counters.as<unsigned long long>() + (bi % 32), st))
+        return rc;
+      if (int rc = big_status(S, st)) return rc;
+    } else if (lr) {
       if (int rc = lr_launch(p->precision, nlim, dense_lists, A->dev(), B->dev(), w, o, p,
                              S.counters.as<unsigned long long>() + (bi % 32), st))
         return rc;
@@ -730,6 +827,36 @@ int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_node
   if (e == cudaSuccess) e = up(c->d_nz_off, nz_off, sizeof(int64_t) * n_graphs);
   if (e == cudaSuccess) e = up(c->d_col, col, sizeof(int32_t) * nz_total);
   if (e == cudaSuccess) e = up(c->d_val, val, sizeof(double) * nz_total);
+  {  // CSC of every graph (rows ascending within a column), same offsets as the CSR
+    std::vector<int32_t> cscp(rp_total, 0), crow(nz_total, 0);
+    std::vector<double> cval(nz_total, 0.0);
+    for (int g = 0; g < n_graphs; g++) {
+      const int n = n_nodes[g];
+      const int32_t *rp = rowptr + rp_off[g];
+      int32_t *cp = cscp.data() + rp_off[g];
+      for (int r = 0; r < n; r++)
+        for (int32_t q = rp[r]; q < rp[r + 1]; q++) {
+          const int cc = col[nz_off[g] + q];
+          if (cc < 0 || cc >= n) {
+            delete c;
+            return fail(CFGSIM_ERR_ARG, "column index out of range in graph " + std::to_string(g));
+          }
+          cp[cc + 1]++;
+        }
+      for (int k = 0; k < n; k++) cp[k + 1] += cp[k];
+      std::vector<int32_t> fill(cp, cp + n);
+      for (int r = 0; r < n; r++)
+        for (int32_t q = rp[r]; q < rp[r + 1]; q++) {
+          const int cc = col[nz_off[g] + q];
+          const int32_t at = fill[cc]++;
+          crow[nz_off[g] + at] = r;
+          cval[nz_off[g] + at] = val[nz_off[g] + q];
+        }
+    }
+    if (e == cudaSuccess) e = up(c->d_cscp, cscp.data(), sizeof(int32_t) * rp_total);
+    if (e == cudaSuccess) e = up(c->d_csc_row, crow.data(), sizeof(int32_t) * nz_total);
+    if (e == cudaSuccess) e = up(c->d_csc_val, cval.data(), sizeof(double) * nz_total);
+  }
   if (e == cudaSuccess) e = up(c->d_perm, c->perm.data(), sizeof(int32_t) * n_graphs);
   if (e == cudaSuccess) e = up(c->d_row_start, c->row_start.data(), sizeof(int64_t) * (n_graphs + 1));
   if (e != cudaSuccess) {
@@ -858,9 +985,13 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
     const int N = c->n_sorted[a];
     int a_end = a;
     Plan pl;
-    if (lr) {
-      if (!lr_supported(p->precision, N))
-        return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds the on-chip tiers of this build");
+    const bool big = lr && !lr_supported(p->precision, N);
+    if (big) {
+      if (N > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
+      while (a_end + 1 < c->K && !lr_supported(p->precision, c->n_sorted[a_end + 1]) &&
+             big_kb(c->n_sorted[a_end + 1]) == big_kb(N))
+        a_end++;
+    } else if (lr) {
       while (a_end + 1 < c->K && c->n_sorted[a_end + 1] == N) a_end++;
     } else {
       pl = plan_for(p->precision, N, false);
@@ -874,7 +1005,9 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
     w.n_items = seg_end - u;
     w.u0 = u;
     unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no % 64);
-    if (lr) {
+    if (big) {
+      if (int rc = big_launch(p->precision, N, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
+    } else if (lr) {
       if (int rc = lr_launch(p->precision, N, false, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
     } else {
       if (int rc = launch_tier(p->precision, pl.ti, N, cap_for(p->precision, pl, N, false), c->dev(), c->dev(),
@@ -887,6 +1020,7 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   }
   // overflowed / ambiguous pairs of all runs (records hold absolute units)
   if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
+  if (int rc = big_status(S, st)) return rc;
   CU(cudaGetLastError());
   return CFGSIM_OK;
 }

@@ -42,6 +42,11 @@ struct DevCorpus {
   const int64_t *nz_off;
   const int32_t *col;
   const double *val;
+  // transposed copy (CSC): graph g's column pointer is cscp[rp_off[g] ..],
+  // its rows / values csc_row/csc_val[nz_off[g] + e], rows ascending
+  const int32_t *cscp;
+  const int32_t *csc_row;
+  const double *csc_val;
 };
 
 enum { WORK_LIST = 0, WORK_TRIANGLE = 1 };

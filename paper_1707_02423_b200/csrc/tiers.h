@@ -3,6 +3,7 @@
 #pragma once
 #include "isorank.cuh"
 #include "isorank_lr.cuh"
+#include "isorank_big.cuh"
 
 #define CFGSIM_TIER_LIST(X)      \
   X(double, 1, 4, 4, 6)          \
@@ -37,7 +38,20 @@
   X(float, 2, 4, 8, 128, 5)   \
   X(float, 4, 4, 8, 512, 1)
 
+#define CFGSIM_EXTERN_BIG(T, KB)                                                              \
+  extern template __global__ void cfgsim::isorank_big_kernel<T, KB>(                         \
+      cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
+      cfgsim::BigParams, unsigned long long *);
+#define CFGSIM_INSTANTIATE_BIG(T, KB)                                                         \
+  template __global__ void cfgsim::isorank_big_kernel<T, KB>(                                \
+      cfgsim::DevCorpus, cfgsim::DevCorpus, cfgsim::PairWork, cfgsim::PairOut,              \
+      cfgsim::BigParams, unsigned long long *);
+// KB = sort chunks per lane: N <= 32 * KB
+#define CFGSIM_BIG_LIST_T(T, X) X(T, 8) X(T, 16) X(T, 32)
+
 #ifndef CFGSIM_TIER_TU
+CFGSIM_BIG_LIST_T(double, CFGSIM_EXTERN_BIG)
+CFGSIM_BIG_LIST_T(float, CFGSIM_EXTERN_BIG)
 CFGSIM_TIER_LIST(CFGSIM_EXTERN_TIER)
 CFGSIM_LR_LIST(CFGSIM_EXTERN_LR)
 #endif
