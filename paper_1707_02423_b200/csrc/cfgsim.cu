@@ -1129,28 +1129,129 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
   OutStage sd, si;
   CU(sd.prepare(best_d, sizeof(double) * nq));
   CU(si.prepare(best_idx, sizeof(int64_t) * nq));
-  // query blocks so that one block's distance matrix stays <= ~2^27 entries
-  const int64_t per_block = std::max<int64_t>(1, ((int64_t)1 << 27) / nc);
-  DBuf dm;
+  Scratch &S = scratch_for(Q->device);
+  if (int rc = ensure_scratch(S, 1 << 16)) return rc;
+  // corpus range in ascending node count (stable): pairs are enumerated as
+  // rectangles of equal N = max(n_q, n_c) (two per distinct N) in these orders
+  std::vector<int32_t> cs(nc);
+  std::iota(cs.begin(), cs.end(), c0);
+  std::stable_sort(cs.begin(), cs.end(), [&](int x, int y) { return C->n_nodes[x] < C->n_nodes[y]; });
+  DBuf dcs;
+  CU(dcs.alloc(sizeof(int32_t) * nc));
+  CU(cudaMemcpyAsync(dcs.p, cs.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
+  // query blocks: one block's distance matrix stays <= 2^28 entries (2 GiB)
+  const int64_t per_block = std::max<int64_t>(1, ((int64_t)1 << 28) / nc);
+  DBuf dm, dqs;
   CU(dm.alloc(sizeof(double) * std::min<int64_t>(nq, per_block) * nc));
+  CU(dqs.alloc(sizeof(int32_t) * std::min<int64_t>(nq, per_block)));
+  const bool lr = use_lowrank();
   for (int32_t q0 = 0; q0 < nq; q0 += (int32_t)per_block) {
     const int32_t q1 = (int32_t)std::min<int64_t>(nq, q0 + per_block);
-    std::vector<int32_t> ia, ib;
-    std::vector<int64_t> sl;
-    ia.reserve((size_t)(q1 - q0) * nc);
-    ib.reserve((size_t)(q1 - q0) * nc);
-    sl.reserve((size_t)(q1 - q0) * nc);
-    for (int32_t q = q0; q < q1; q++)
-      for (int32_t j = 0; j < nc; j++) {
-        ia.push_back(q);
-        ib.push_back(c0 + j);
-        sl.push_back((int64_t)(q - q0) * nc + j);
+    const int32_t bq = q1 - q0;
+    std::vector<int32_t> qs(bq);
+    std::iota(qs.begin(), qs.end(), q0);
+    std::stable_sort(qs.begin(), qs.end(), [&](int x, int y) { return Q->n_nodes[x] < Q->n_nodes[y]; });
+    CU(cudaMemcpyAsync(dqs.p, qs.data(), sizeof(int32_t) * bq, cudaMemcpyHostToDevice, st));
+    // launches: one per exact N (low-rank kernel) / per sort class (large-N kernel)
+    struct Launch { int key, nlim; std::vector<int32_t> rects; };
+    std::vector<Launch> launches;
+    std::vector<int> ns;
+    for (int x : qs) ns.push_back(Q->n_nodes[x]);
+    for (int x : cs) ns.push_back(C->n_nodes[x]);
+    std::sort(ns.begin(), ns.end());
+    ns.erase(std::unique(ns.begin(), ns.end()), ns.end());
+    auto qcount = [&](int n, bool le) {  // queries with n_q < n (le: <= n)
+      return (int32_t)((le ? std::upper_bound(qs.begin(), qs.end(), n, [&](int v, int x) { return v < Q->n_nodes[x]; })
+                           : std::lower_bound(qs.begin(), qs.end(), n, [&](int x, int v) { return Q->n_nodes[x] < v; })) -
+                       qs.begin());
+    };
+    auto ccount = [&](int n, bool le) {
+      return (int32_t)((le ? std::upper_bound(cs.begin(), cs.end(), n, [&](int v, int x) { return v < C->n_nodes[x]; })
+                           : std::lower_bound(cs.begin(), cs.end(), n, [&](int x, int v) { return C->n_nodes[x] < v; })) -
+                       cs.begin());
+    };
+    for (int N : ns) {
+      if (N > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
+      const int key = (!lr || lr_supported(p->precision, N)) ? N : kBigKey + big_kb(N);
+      if (launches.empty() || launches.back().key != key) launches.push_back({key, N, {}});
+      Launch &L = launches.back();
+      L.nlim = std::max(L.nlim, N);
+      const int32_t qlt = qcount(N, false), qle = qcount(N, true);
+      const int32_t clt = ccount(N, false), cle = ccount(N, true);
+      if (qle > qlt && cle > 0) L.rects.insert(L.rects.end(), {qlt, qle, 0, cle});   // n_q == N, n_c <= N
+      if (qlt > 0 && cle > clt) L.rects.insert(L.rects.end(), {0, qlt, clt, cle});   // n_q < N, n_c == N
+    }
+    for (size_t li = 0; li < launches.size(); li++) {
+      Launch &L = launches[li];
+      const int nr = (int)L.rects.size() / 4;
+      if (nr == 0) continue;
+      std::vector<int64_t> rs(nr + 1, 0);
+      for (int r = 0; r < nr; r++)
+        rs[r + 1] = rs[r] + (int64_t)(L.rects[4 * r + 1] - L.rects[4 * r]) * (L.rects[4 * r + 3] - L.rects[4 * r + 2]);
+      DBuf drs, drect;
+      CU(drs.alloc(sizeof(int64_t) * (nr + 1)));
+      CU(drect.alloc(sizeof(int32_t) * 4 * nr));
+      CU(cudaMemcpyAsync(drs.p, rs.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(drect.p, L.rects.data(), sizeof(int32_t) * 4 * nr, cudaMemcpyHostToDevice, st));
+      PairWork w{};
+      w.mode = WORK_RECT;
+      w.n_items = rs[nr];
+      w.nrect = nr;
+      w.rect_start = drs.as<int64_t>();
+      w.rect = drect.as<int32_t>();
+      w.qperm = dqs.as<int32_t>();
+      w.cperm = dcs.as<int32_t>();
+      w.qbase = q0;
+      w.cbase = c0;
+      w.ld = nc;
+      PairOut o{};
+      o.d = dm.as<double>();
+      o.ovf_count = S.ovf_count.as<int32_t>();
+      o.ovf_list = S.ovf_list.as<int64_t>();
+      o.ovf_cap = (int32_t)S.ovf_cap;
+      unsigned long long *ctr = S.counters.as<unsigned long long>() + (li % 64);
+      if (L.key >= kBigKey) {
+        if (int rc = big_launch(p->precision, L.nlim, Q->dev(), C->dev(), w, o, p, ctr, st)) return rc;
+      } else if (lr) {
+        if (int rc = lr_launch(p->precision, L.nlim, false, Q->dev(), C->dev(), w, o, p, ctr, st)) return rc;
+      } else {
+        const Plan pl = plan_for(p->precision, L.nlim, false);
+        if (pl.ti < 0) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(L.nlim) + " exceeds the on-chip tiers");
+        if (int rc = launch_tier(p->precision, pl.ti, L.nlim, cap_for(p->precision, pl, L.nlim, false), Q->dev(),
+                                 C->dev(), w, o, p, ctr, st))
+          return rc;
       }
-    if (int rc = run_list(Q, C, ia, ib, sl, p, dm.as<double>(), nullptr, nullptr, nullptr, nullptr,
-                          nullptr, nullptr, st))
-      return rc;
-    rowmin_kernel<<<q1 - q0, 256, 0, st>>>(q1 - q0, nc, dm.as<double>(), c0,
-                                           (double *)sd.dev + q0, (int64_t *)si.dev + q0);
+      // overflowed / ambiguous items of this launch: re-run as pair lists
+      int32_t cnt = 0;
+      CU(cudaMemcpyAsync(&cnt, S.ovf_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (cnt > 0) {
+        if (cnt > S.ovf_cap) return fail(CFGSIM_ERR_CUDA, "overflow list capacity exceeded");
+        std::vector<int64_t> recs(cnt);
+        CU(cudaMemcpy(recs.data(), S.ovf_list.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+        CU(cudaMemset(S.ovf_count.p, 0, sizeof(int32_t)));
+        std::vector<int32_t> ra[2], rb[2];
+        std::vector<int64_t> rsl[2];
+        for (int64_t rec : recs) {
+          const int kind = (int)(rec & 1);
+          const int64_t item = rec >> 2;
+          const int r = (int)(std::upper_bound(rs.begin(), rs.end(), item) - rs.begin()) - 1;
+          const int32_t *R = L.rects.data() + 4 * r;
+          const int64_t loc = item - rs[r];
+          const int wdt = R[3] - R[2];
+          const int gq = qs[R[0] + (int)(loc / wdt)], gc = cs[R[2] + (int)(loc % wdt)];
+          ra[kind].push_back(gq);
+          rb[kind].push_back(gc);
+          rsl[kind].push_back((int64_t)(gq - q0) * nc + (gc - c0));
+        }
+        for (int kind = 0; kind < 2; kind++)
+          if (int rc = run_list(Q, C, ra[kind], rb[kind], rsl[kind], p, dm.as<double>(), nullptr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, st, kind == 0 ? 1 : 2))
+            return rc;
+      }
+    }
+    if (int rc = big_status(S, st)) return rc;
+    rowmin_kernel<<<bq, 256, 0, st>>>(bq, nc, dm.as<double>(), c0, (double *)sd.dev + q0, (int64_t *)si.dev + q0);
     CU(cudaGetLastError());
   }
   CU(sd.finish(st));

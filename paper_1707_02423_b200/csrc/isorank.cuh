@@ -49,7 +49,7 @@ struct DevCorpus {
   const double *csc_val;
 };
 
-enum { WORK_LIST = 0, WORK_TRIANGLE = 1 };
+enum { WORK_LIST = 0, WORK_TRIANGLE = 1, WORK_RECT = 2 };
 
 struct PairWork {
   int32_t mode;
@@ -65,7 +65,64 @@ struct PairWork {
   const int64_t *row_start;  // K+1
   const int32_t *perm;       // sorted position -> graph index
   int32_t K;
+  // rect mode (query x corpus): item -> rectangle r (rect_start prefix),
+  // rect[4r..4r+3] = q0, q1, c0, c1 in size-sorted positions of the two
+  // corpora; output slot = (qperm[q] - qbase) * ld + (cperm[c] - cbase)
+  int32_t nrect;
+  const int64_t *rect_start;
+  const int32_t *rect;
+  const int32_t *qperm;
+  const int32_t *cperm;
+  int32_t qbase, cbase;
+  int64_t ld;
 };
+
+// Work item -> (ga, gb, number of directions, first output slot).  Triangle
+// mode computes one alignment per unordered pair in the caller's (lower
+// index, higher index) direction — the reference's upper triangle — so
+// results do not depend on the size-sorted schedule; `ordered` computes both.
+__device__ __forceinline__ void decode_item(const PairWork &work, int64_t item, int &ga, int &gb, int &ndir,
+                                            int64_t &slot0) {
+  ndir = 1;
+  if (work.mode == WORK_LIST) {
+    ga = work.ia[item];
+    gb = work.ib[item];
+    slot0 = work.slot ? work.slot[item] : item;
+    return;
+  }
+  if (work.mode == WORK_RECT) {
+    int lo = 0, hi = work.nrect - 1;  // last r with rect_start[r] <= item
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (work.rect_start[mid] <= item) lo = mid; else hi = mid - 1;
+    }
+    const int32_t *R = work.rect + 4 * lo;
+    const int64_t loc = item - work.rect_start[lo];
+    const int w = R[3] - R[2];
+    const int q = R[0] + (int)(loc / w), c = R[2] + (int)(loc % w);
+    ga = work.qperm[q];
+    gb = work.cperm[c];
+    slot0 = (int64_t)(ga - work.qbase) * work.ld + (gb - work.cbase);
+    return;
+  }
+  const int64_t u = work.u0 + item;
+  int lo = 0, hi = work.K - 1;  // largest a with row_start[a] <= u
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (work.row_start[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  const int a = lo;
+  const int b = a + (int)(u - work.row_start[a]);
+  ga = work.perm[a];
+  gb = work.perm[b];
+  if (work.ordered) {
+    slot0 = 2 * (u - work.out_base);
+    ndir = (a == b) ? 1 : 2;
+  } else {
+    if (ga > gb) { const int t = ga; ga = gb; gb = t; }
+    slot0 = u - work.out_base;
+  }
+}
 
 struct PairOut {
   double *d;
@@ -850,34 +907,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     if (item >= work.n_items) break;
 
     // ---- decode the work item
-    int ga, gb, ndir = 1;
+    int ga, gb, ndir;
     int64_t slot0;
-    if (work.mode == WORK_LIST) {
-      ga = work.ia[item];
-      gb = work.ib[item];
-      slot0 = work.slot ? work.slot[item] : item;
-    } else {
-      const int64_t u = work.u0 + item;
-      int lo = 0, hi = work.K - 1;  // largest a with row_start[a] <= u
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (work.row_start[mid] <= u) lo = mid; else hi = mid - 1;
-      }
-      const int a = lo;
-      const int b = a + (int)(u - work.row_start[a]);
-      ga = work.perm[a];
-      gb = work.perm[b];
-      if (work.ordered) {
-        slot0 = 2 * (u - work.out_base);
-        ndir = (a == b) ? 1 : 2;
-      } else {
-        // one alignment per unordered pair, always in the caller's (lower
-        // index, higher index) direction — the reference's upper triangle —
-        // so results do not depend on the size-sorted schedule
-        if (ga > gb) { const int t = ga; ga = gb; gb = t; }
-        slot0 = u - work.out_base;
-      }
-    }
+    decode_item(work, item, ga, gb, ndir, slot0);
 
     for (int dir = 0; dir < ndir; dir++) {
       const int g1 = dir ? gb : ga, g2 = dir ? ga : gb;

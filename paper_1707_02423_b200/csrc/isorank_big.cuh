@@ -35,8 +35,9 @@ namespace cfgsim {
 
 constexpr int BIG_THREADS = 256;
 constexpr int BIG_WARPS = BIG_THREADS / 32;
-constexpr int BIG_TM = 128, BIG_TN = 64, BIG_KC = 8;  // GEMM tile and k-chunk
+constexpr int BIG_TM = 128, BIG_TN = 64, BIG_KC = 16;  // GEMM tile and k-chunk
 constexpr int BIG_CB = 10;                            // column bits of a sort key (N <= 1024)
+constexpr int BIG_R = 1024 / BIG_THREADS;             // greedy rows per thread
 
 struct BigParams {
   double alpha;
@@ -52,7 +53,7 @@ struct BigParams {
 
 // per-CTA global slab
 struct BigSlab {
-  size_t coef, uh, vh, x, ord, total;
+  size_t coef, uh, vh, x, skey, total;
 };
 
 template <typename T>
@@ -68,7 +69,7 @@ __host__ __device__ inline BigSlab big_slab_layout(int nlim, int kcap) {
   s.uh = take(sizeof(T) * (size_t)(kcap + 1) * nlim);
   s.vh = take(sizeof(T) * (size_t)(kcap + 1) * nlim);
   s.x = take(sizeof(T) * (size_t)nlim * nlim);
-  s.ord = take(sizeof(uint16_t) * (size_t)nlim * nlim);
+  s.skey = take(sizeof(unsigned long long) * (size_t)nlim * nlim);
   s.total = o;
   return s;
 }
@@ -80,7 +81,7 @@ struct BigSmem {
   // gemm region
   size_t us, vs;
   // greedy region
-  size_t hptr, hcol, hval, mrow;
+  size_t taken, gslot, mrow;
   size_t red, misc, total;
 };
 
@@ -94,7 +95,7 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
     return at;
   };
   s.red = take(sizeof(double) * 2 * BIG_WARPS * 4);
-  s.misc = take(128);
+  s.misc = take(256);
   const size_t base = o;
   for (int d = 0; d < 2; d++) {
     s.lo[d] = take(sizeof(int16_t) * nlim);
@@ -108,48 +109,18 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
   s.scr = take(sizeof(double) * 2 * nlim);  // operator build scratch (colW, rowAW)
   const size_t sweep_end = o;
   o = base;
-  s.us = take(sizeof(T) * BIG_KC * BIG_TM);
-  s.vs = take(sizeof(T) * BIG_KC * BIG_TN);
+  s.us = take(sizeof(T) * 2 * BIG_KC * BIG_TM);  // double-buffered
+  s.vs = take(sizeof(T) * 2 * BIG_KC * BIG_TN);
   const size_t gemm_end = o;
   o = base;
-  s.hptr = take(sizeof(uint16_t) * nlim);
-  s.hcol = take(sizeof(uint16_t) * nlim);
-  s.hval = take(sizeof(T) * nlim);
+  s.taken = take(sizeof(uint32_t) * 32);
+  s.gslot = take(sizeof(unsigned long long) * 2 * BIG_WARPS + sizeof(int32_t) * (4 * BIG_WARPS + 2));
   s.mrow = take(sizeof(int32_t) * nlim);
   const size_t greedy_end = o;
   size_t e = sweep_end > gemm_end ? sweep_end : gemm_end;
   e = e > greedy_end ? e : greedy_end;
   s.total = e;
   return s;
-}
-
-// Decode work item -> (ga, gb, number of directions, first output slot).
-__device__ __forceinline__ void decode_item(const PairWork &work, int64_t item, int &ga, int &gb, int &ndir,
-                                            int64_t &slot0) {
-  ndir = 1;
-  if (work.mode == WORK_LIST) {
-    ga = work.ia[item];
-    gb = work.ib[item];
-    slot0 = work.slot ? work.slot[item] : item;
-    return;
-  }
-  const int64_t u = work.u0 + item;
-  int lo = 0, hi = work.K - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (work.row_start[mid] <= u) lo = mid; else hi = mid - 1;
-  }
-  const int a = lo;
-  const int b = a + (int)(u - work.row_start[a]);
-  ga = work.perm[a];
-  gb = work.perm[b];
-  if (work.ordered) {
-    slot0 = 2 * (u - work.out_base);
-    ndir = (a == b) ? 1 : 2;
-  } else {
-    if (ga > gb) { const int t = ga; ga = gb; gb = t; }
-    slot0 = u - work.out_base;
-  }
 }
 
 // One side's operator, as the sweep phases see it.
@@ -290,6 +261,94 @@ __device__ __forceinline__ unsigned long long big_sort_key(T v, int col, int emi
   }
 }
 
+template <typename T>
+__device__ __forceinline__ int big_exponent(T v) {
+  return (sizeof(T) == 8) ? (int)((__double_as_longlong((double)v) >> 52) & 0x7ff)
+                          : (int)((__float_as_uint((float)v) >> 23) & 0xff);
+}
+
+template <typename T>
+__device__ __forceinline__ unsigned long long big_bits(T v) {
+  return (sizeof(T) == 8) ? (unsigned long long)__double_as_longlong((double)v)
+                          : (unsigned long long)__float_as_uint((float)v);
+}
+
+__device__ __forceinline__ int big_key_col(unsigned long long k) {
+  return (1 << BIG_CB) - 1 - (int)(k & ((1ull << BIG_CB) - 1));
+}
+
+__device__ __forceinline__ void big_cp_async8(void *smem_dst, const void *gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+__device__ __forceinline__ void big_cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// B-byte async copy global -> shared; zero-fills the destination when !valid
+template <int B>
+__device__ __forceinline__ void big_cp_async_zfill(void *smem_dst, const void *gsrc, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int n = valid ? B : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc), "n"(B), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void big_cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int G>
+__device__ __forceinline__ void big_cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(G) : "memory"); }
+
+// compare-exchange of registers c and c ^ J inside each lane (elements
+// e = lane * KB + c), direction by bit k of e
+template <int KB, int J>
+__device__ __forceinline__ void big_stage_reg(unsigned long long (&v)[KB], int lane, int k) {
+#pragma unroll
+  for (int c = 0; c < KB; c++) {
+    if ((c & J) == 0) {
+      const int pc = c | J;
+      const bool up = (((lane * KB + c) & k) == 0);
+      const unsigned long long a = v[c], b = v[pc];
+      const bool sw = up ? (b > a) : (a > b);
+      v[c] = sw ? b : a;
+      v[pc] = sw ? a : b;
+    }
+  }
+}
+
+// Warp bitonic sort of 32*KB distinct keys, descending; element e = lane*KB + c
+// (each lane holds a contiguous run, so only log2(32) of every merge's stages
+// cross lanes).  Stage loops stay rolled: the fully unrolled 1024-key network
+// does not fit the instruction cache.
+template <int KB>
+__device__ __forceinline__ void big_sort_desc(unsigned long long (&v)[KB], int lane) {
+  constexpr int n = 32 * KB;
+#pragma unroll 1
+  for (int k = 2; k <= n; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= KB) {
+        const int lm = j / KB;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int c = 0; c < KB; c++) {
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[c], lm);
+          const bool up = (((lane * KB + c) & k) == 0);
+          const unsigned long long hi = o > v[c] ? o : v[c], lo = o > v[c] ? v[c] : o;
+          v[c] = (lower == up) ? hi : lo;
+        }
+      } else {
+        switch (j) {
+          case 1: big_stage_reg<KB, 1>(v, lane, k); break;
+          case 2: if constexpr (KB > 2) big_stage_reg<KB, 2>(v, lane, k); break;
+          case 4: if constexpr (KB > 4) big_stage_reg<KB, 4>(v, lane, k); break;
+          case 8: if constexpr (KB > 8) big_stage_reg<KB, 8>(v, lane, k); break;
+          case 16: if constexpr (KB > 16) big_stage_reg<KB, 16>(v, lane, k); break;
+          default: break;
+        }
+      }
+    }
+  }
+}
+
 template <typename T, int KB>
 __global__ void __launch_bounds__(BIG_THREADS, 2)
     isorank_big_kernel(DevCorpus CA, DevCorpus CB, PairWork work, PairOut out, BigParams prm,
@@ -302,10 +361,9 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
   T *Uh = (T *)(slab + G.uh);
   T *Vh = (T *)(slab + G.vh);
   T *X = (T *)(slab + G.x);
-  uint16_t *ord = (uint16_t *)(slab + G.ord);
+  unsigned long long *skey = (unsigned long long *)(slab + G.skey);
   double *red = (double *)(smem_raw + L.red);
   int64_t *s_item = (int64_t *)(smem_raw + L.misc);
-  double *s_scr = (double *)(smem_raw + L.misc + 16);  // 2 doubles
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = BIG_THREADS;
@@ -328,12 +386,8 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       const int N = na > nb ? na : nb;
 
       // ---- 1. operators
-      BigSide SD[2];
-#pragma unroll
-      for (int s = 0; s < 2; s++) {
-        const DevCorpus &Cs = s ? C2 : C1;
-        const int g = s ? g2 : g1;
-        BigSide &S = SD[s];
+      BigSide SA, SB;
+      auto setup = [&](BigSide &S, const DevCorpus &Cs, int g, int sd) {
         S.n = Cs.n_nodes[g];
         S.N = N;
         S.kind = (S.n == N) ? 0 : (S.n == 1 ? 2 : 1);
@@ -343,13 +397,15 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         S.cp = Cs.cscp + Cs.rp_off[g];
         S.cr = Cs.csc_row + Cs.nz_off[g];
         S.cv = Cs.csc_val + Cs.nz_off[g];
-        S.lo = (int16_t *)(smem_raw + L.lo[s]);
-        S.fr = (double *)(smem_raw + L.fr[s]);
-        S.rinv = (double *)(smem_raw + L.rinv[s]);
-        S.pst = (int16_t *)(smem_raw + L.pst[s]);
-        S.zf = (uint8_t *)(smem_raw + L.zf[s]);
+        S.lo = (int16_t *)(smem_raw + L.lo[sd]);
+        S.fr = (double *)(smem_raw + L.fr[sd]);
+        S.rinv = (double *)(smem_raw + L.rinv[sd]);
+        S.pst = (int16_t *)(smem_raw + L.pst[sd]);
+        S.zf = (uint8_t *)(smem_raw + L.zf[sd]);
         big_build_side(S, (double *)(smem_raw + L.scr));
-      }
+      };
+      setup(SA, C1, g1, 0);
+      setup(SB, C2, g2, 1);
       T *ring[2] = {(T *)(smem_raw + L.ring[0]), (T *)(smem_raw + L.ring[1])};
       T *tv[2] = {(T *)(smem_raw + L.t[0]), (T *)(smem_raw + L.t[1])};
 
@@ -360,7 +416,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         Uh[q] = (T)1;
         Vh[q] = (T)1;
       }
-      double zsum[2] = {SD[0].zcount, SD[1].zcount};
+      double zsum[2] = {SA.zcount, SB.zcount};
       const double invN = 1.0 / (double)N;
       const double inv_nn = 1.0 / (double)((long long)N * N);
       const double c = (1.0 - prm.alpha) * inv_nn;  // (1-alpha)*uniform, similarity.py:140
@@ -373,26 +429,38 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         const int cur = (k - 1) & 1, nxt = k & 1;  // ring slots of u_{k-1}, u_k
         // phase 1: t = A^T W^T D^-1 u_{k-1}
         {
-          const int n0 = SD[0].kind == 2 ? 0 : SD[0].n;
-          const int n1 = SD[1].kind == 2 ? 0 : SD[1].n;
+          const int n0 = SA.kind == 2 ? 0 : SA.n;
+          const int n1 = SB.kind == 2 ? 0 : SB.n;
           for (int q = tid; q < n0 + n1; q += NT) {
             if (q < n0)
-              tv[0][q] = big_t_entry<T>(SD[0], ring[0] + cur * N, q);
+              tv[0][q] = big_t_entry<T>(SA, ring[0] + cur * N, q);
             else
-              tv[1][q - n0] = big_t_entry<T>(SD[1], ring[1] + cur * N, q - n0);
+              tv[1][q - n0] = big_t_entry<T>(SB, ring[1] + cur * N, q - n0);
           }
         }
         __syncthreads();
         // phase 2: u_k = W t + zsum/N; partial sums of |u_k - u_{k-1}| and z^T u_k
         double part[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int q = tid; q < 2 * N; q += NT) {
-          const int s = q >= N, i = q - s * N;
-          const T un = big_u_entry<T>(SD[s], tv[s], i, zsum[s] * invN);
-          const T uo = ring[s][cur * N + i];
-          ring[s][nxt * N + i] = un;
-          if (k <= prm.kcap) (s ? Vh : Uh)[(size_t)k * N + i] = un;
-          part[2 * s] += fabs((double)un - (double)uo);
-          if (SD[s].zf[i]) part[2 * s + 1] += (double)un;
+        {
+          const double za = zsum[0] * invN, zb = zsum[1] * invN;
+          for (int q = tid; q < 2 * N; q += NT) {
+            if (q < N) {
+              const T un = big_u_entry<T>(SA, tv[0], q, za);
+              const T uo = ring[0][cur * N + q];
+              ring[0][nxt * N + q] = un;
+              if (k <= prm.kcap) Uh[(size_t)k * N + q] = un;
+              part[0] += fabs((double)un - (double)uo);
+              if (SA.zf[q]) part[1] += (double)un;
+            } else {
+              const int i = q - N;
+              const T un = big_u_entry<T>(SB, tv[1], i, zb);
+              const T uo = ring[1][cur * N + i];
+              ring[1][nxt * N + i] = un;
+              if (k <= prm.kcap) Vh[(size_t)k * N + i] = un;
+              part[2] += fabs((double)un - (double)uo);
+              if (SB.zf[i]) part[3] += (double)un;
+            }
+          }
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) {
@@ -467,11 +535,40 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       }
       __syncthreads();
 
-      // ---- 3. X = sum_m coef_m u_m v_m^T  (128 x 64 tiles, 8 x 4 per thread)
+      // ---- 3. X = sum_m coef_m u_m v_m^T  (128 x 64 tiles, 8 x 4 per thread,
+      //         k-chunks of the histories double-buffered with cp.async);
+      //         exponent range of X for the pair-wide sort keys.
+      //         u_m is pre-scaled by coef_m in place (the product the
+      //         low-rank kernel forms as cak * u).
+      for (int e = tid; e < (K + 1) * N; e += NT) Uh[e] = coef[e / N] * Uh[e];
+      __syncthreads();
+      int emin = 0x7fffffff, emax = -1;
       {
         T *Us = (T *)(smem_raw + L.us);
         T *Vs = (T *)(smem_raw + L.vs);
         const int ty = tid >> 4, tx = tid & 15;
+        const int nch = (K + BIG_KC) / BIG_KC;  // chunks covering m = 0..K
+        auto stage = [&](int i0, int j0, int ch, int bufi) {
+          T *us = Us + bufi * BIG_KC * BIG_TM, *vs = Vs + bufi * BIG_KC * BIG_TN;
+          for (int e = tid; e < BIG_KC * (BIG_TM + BIG_TN); e += NT) {
+            int mm, x, lim;
+            const T *src;
+            T *dst;
+            if (e < BIG_KC * BIG_TM) {
+              mm = e / BIG_TM; x = e % BIG_TM; lim = N - i0;
+              src = Uh + (size_t)(ch * BIG_KC + mm) * N + i0 + x;
+              dst = us + e;
+            } else {
+              const int f = e - BIG_KC * BIG_TM;
+              mm = f / BIG_TN; x = f % BIG_TN; lim = N - j0;
+              src = Vh + (size_t)(ch * BIG_KC + mm) * N + j0 + x;
+              dst = vs + f;
+            }
+            const bool ok = (ch * BIG_KC + mm <= K) && x < lim;
+            big_cp_async_zfill<sizeof(T)>(dst, ok ? (const void *)src : (const void *)Uh, ok);
+          }
+          big_cp_async_commit();
+        };
         for (int i0 = 0; i0 < N; i0 += BIG_TM)
           for (int j0 = 0; j0 < N; j0 += BIG_TN) {
             T acc[8][4];
@@ -479,29 +576,30 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
             for (int a = 0; a < 8; a++)
 #pragma unroll
               for (int b = 0; b < 4; b++) acc[a][b] = (T)0;
-            for (int m0 = 0; m0 <= K; m0 += BIG_KC) {
-              __syncthreads();
-              for (int e = tid; e < BIG_KC * BIG_TM; e += NT) {
-                const int mm = e / BIG_TM, i = e % BIG_TM, m = m0 + mm;
-                Us[e] = (m <= K && i0 + i < N) ? coef[m] * Uh[(size_t)m * N + i0 + i] : (T)0;
+            __syncthreads();  // previous tile done with both buffers
+            stage(i0, j0, 0, 0);
+            for (int ch = 0; ch < nch; ch++) {
+              if (ch + 1 < nch) {
+                stage(i0, j0, ch + 1, (ch + 1) & 1);
+                big_cp_async_wait_group<1>();
+              } else {
+                big_cp_async_wait_group<0>();
               }
-              for (int e = tid; e < BIG_KC * BIG_TN; e += NT) {
-                const int mm = e / BIG_TN, j = e % BIG_TN, m = m0 + mm;
-                Vs[e] = (m <= K && j0 + j < N) ? Vh[(size_t)m * N + j0 + j] : (T)0;
-              }
               __syncthreads();
+              const T *us = Us + (ch & 1) * BIG_KC * BIG_TM, *vs = Vs + (ch & 1) * BIG_KC * BIG_TN;
 #pragma unroll
               for (int mm = 0; mm < BIG_KC; mm++) {
                 T ua[8], vb[4];
 #pragma unroll
-                for (int a = 0; a < 8; a++) ua[a] = Us[mm * BIG_TM + ty + 16 * a];
+                for (int a = 0; a < 8; a++) ua[a] = us[mm * BIG_TM + ty + 16 * a];
 #pragma unroll
-                for (int b = 0; b < 4; b++) vb[b] = Vs[mm * BIG_TN + tx + 16 * b];
+                for (int b = 0; b < 4; b++) vb[b] = vs[mm * BIG_TN + tx + 16 * b];
 #pragma unroll
                 for (int a = 0; a < 8; a++)
 #pragma unroll
                   for (int b = 0; b < 4; b++) acc[a][b] = fma(ua[a], vb[b], acc[a][b]);
               }
+              __syncthreads();  // buffer (ch & 1) is re-staged by chunk ch + 2
             }
 #pragma unroll
             for (int a = 0; a < 8; a++) {
@@ -509,163 +607,241 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
 #pragma unroll
               for (int b = 0; b < 4; b++) {
                 const int j = j0 + tx + 16 * b;
-                if (i < N && j < N) X[(size_t)i * N + j] = acc[a][b];
+                if (i < N && j < N) {
+                  X[(size_t)i * N + j] = acc[a][b];
+                  const int e = big_exponent(acc[a][b]);
+                  emin = min(emin, e);
+                  emax = max(emax, e);
+                }
               }
             }
           }
       }
-      __syncthreads();
-
-      // ---- 4a. row orders (value desc, column asc) as packed keys
-      for (int i = warp; i < N; i += BIG_WARPS) {
-        const T *row = X + (size_t)i * N;
-        int emin = 0x7fffffff, emax = -1;
-        for (int j = lane; j < N; j += 32) {
-          const int e = (sizeof(T) == 8) ? (int)((__double_as_longlong((double)row[j]) >> 52) & 0x7ff)
-                                         : (int)((__float_as_uint((float)row[j]) >> 23) & 0xff);
-          emin = min(emin, e);
-          emax = max(emax, e);
-        }
+      {
+        int *ered = (int *)(smem_raw + L.misc + 32);
         emin = __reduce_min_sync(0xffffffffu, emin);
         emax = __reduce_max_sync(0xffffffffu, emax);
-        int shift = 0;  // low mantissa bits dropped so exponent|mantissa|column fits 64 bits
-        if (sizeof(T) == 8) {
-          const int eb = 32 - __clz(emax - emin);
-          shift = eb + 52 + BIG_CB - 64;
-          if (shift < 0) shift = 0;
+        if (lane == 0) {
+          ered[warp] = emin;
+          ered[BIG_WARPS + warp] = emax;
         }
+        __syncthreads();
+        for (int w = 0; w < BIG_WARPS; w++) {
+          emin = min(emin, ered[w]);
+          emax = max(emax, ered[BIG_WARPS + w]);
+        }
+      }
+      // low mantissa bits dropped so that (rebased exponent | mantissa | column)
+      // fits 64 bits; the same base for every row keeps keys comparable across rows
+      int shift = 0;
+      if (sizeof(T) == 8) {
+        shift = (32 - __clz(emax - emin)) + 52 + BIG_CB - 64;
+        if (shift < 0) shift = 0;
+      }
+      __syncthreads();
+
+      // ---- 4a. row orders (value desc, column asc): warp bitonic sort of keys
+      for (int i = warp; i < N; i += BIG_WARPS) {
+        const T *row = X + (size_t)i * N;
         unsigned long long key[KB];
 #pragma unroll
-        for (int cc = 0; cc < KB; cc++) {
-          const int j = lane + 32 * cc;
-          key[cc] = (j < N) ? big_sort_key<T>(row[j], j, emin, shift) : 0ull;  // padding sorts last
+        for (int c = 0; c < KB; c++) {
+          const int j = lane * KB + c;
+          key[c] = (j < N) ? big_sort_key<T>(row[j], j, emin, shift) : 0ull;  // padding sorts last
         }
-        warp_sort_keys_desc<KB>(key, lane);
-        uint16_t *o = ord + (size_t)i * N;
+        big_sort_desc<KB>(key, lane);
+        unsigned long long *o = skey + (size_t)i * N;
         bool tie = false;
 #pragma unroll
-        for (int cc = 0; cc < KB; cc++) {
-          const int pos = lane + 32 * cc;  // sorted position of key[cc]
-          const int col = (1 << BIG_CB) - 1 - (int)(key[cc] & ((1ull << BIG_CB) - 1));
-          if (pos < N) o[pos] = (uint16_t)col;
-          if (shift > 0) {
-            // neighbour at pos + 1: lane + 1 of this chunk, or lane 0 of the next
-            unsigned long long nk = __shfl_down_sync(0xffffffffu, key[cc], 1);
-            const unsigned long long n0 = __shfl_sync(0xffffffffu, key[cc + 1 < KB ? cc + 1 : cc], 0);
-            if (lane == 31) nk = n0;
-            if (pos + 1 < N && (key[cc] >> BIG_CB) == (nk >> BIG_CB)) {
-              // equal truncated value: misordered only if the exact values differ
-              const int ncol = (1 << BIG_CB) - 1 - (int)(nk & ((1ull << BIG_CB) - 1));
-              if (row[col] != row[ncol]) tie = true;
-            }
+        for (int c = 0; c < KB; c++) {
+          const int pos = lane * KB + c;
+          if (pos < N) o[pos] = key[c];
+          if (shift > 0 && c + 1 < KB && pos + 1 < N && (key[c] >> BIG_CB) == (key[c + 1] >> BIG_CB)) {
+            // equal truncated value: misordered only if the exact values differ
+            if (row[big_key_col(key[c])] != row[big_key_col(key[c + 1])]) tie = true;
           }
+        }
+        if (shift > 0) {  // chunk boundary: last of this lane vs first of the next lane
+          const unsigned long long nk = __shfl_down_sync(0xffffffffu, key[0], 1);
+          const int pos = lane * KB + KB - 1;
+          if (lane < 31 && pos + 1 < N && (key[KB - 1] >> BIG_CB) == (nk >> BIG_CB) &&
+              row[big_key_col(key[KB - 1])] != row[big_key_col(nk)])
+            tie = true;
         }
         __syncwarp();
         if (__any_sync(0xffffffffu, tie) && lane == 0) {
           // insertion pass on exact (value desc, column asc); keys are already
           // ordered up to the dropped bits, so only near-tied runs move
           for (int p = 1; p < N; p++) {
-            const int cp = o[p];
+            const unsigned long long kp = o[p];
+            const int cp = big_key_col(kp);
             const T vp = row[cp];
             int q = p - 1;
             while (q >= 0) {
-              const int cq = o[q];
+              const unsigned long long kq = o[q];
+              const int cq = big_key_col(kq);
               const T vq = row[cq];
               if (vq > vp || (vq == vp && cq < cp)) break;
-              o[q + 1] = (uint16_t)cq;
+              o[q + 1] = kq;
               q--;
             }
-            o[q + 1] = (uint16_t)cp;
+            o[q + 1] = kp;
           }
         }
         __syncwarp();
       }
       __syncthreads();
 
-      // ---- 4b. greedy matching rounds (warp 0), similarity.py:96-108
+      // ---- 4b. greedy matching rounds, similarity.py:96-108, whole CTA.
+      // Thread t owns rows t + 256 r (r < BIG_R).  Each active row's head is
+      // its best untaken column, held as a sort key (comparable across rows
+      // up to the dropped bits; equal truncated heads are resolved on exact
+      // values).  A round: per-warp best head -> shared slots -> every
+      // thread picks the same winner (value desc, row asc = np.argmax's
+      // first occurrence); rows whose head column was taken advance along
+      // their sorted keys (next key already loaded into a register).
       {
-        uint16_t *hptr = (uint16_t *)(smem_raw + L.hptr);
-        uint16_t *hcol = (uint16_t *)(smem_raw + L.hcol);
-        T *hval = (T *)(smem_raw + L.hval);
+        uint32_t *taken = (uint32_t *)(smem_raw + L.taken);
+        unsigned long long *slot_k = (unsigned long long *)(smem_raw + L.gslot);
+        int32_t *slot_r = (int32_t *)(slot_k + 2 * BIG_WARPS);
+        int32_t *slot_n = slot_r + 2 * BIG_WARPS;
         int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
-        if (warp == 0) {
-          uint32_t act = 0u;     // bit c: row lane + 32c active
-          uint32_t taken = 0u;   // bit w of lane l: column 32 l + w taken (this lane's word)
+        for (int w = tid; w < 32; w += NT) taken[w] = 0u;
+        unsigned long long hk[BIG_R], nk[BIG_R];
+        int ptr[BIG_R];
+        uint32_t act = 0u;
 #pragma unroll
-          for (int cc = 0; cc < KB; cc++) {
-            const int i = lane + 32 * cc;
-            if (i < N) {
-              act |= 1u << cc;
-              const int c0 = ord[(size_t)i * N];
-              hptr[i] = 0;
-              hcol[i] = (uint16_t)c0;
-              hval[i] = X[(size_t)i * N + c0];
-            }
+        for (int r = 0; r < BIG_R; r++) {
+          const int i = tid + BIG_THREADS * r;
+          hk[r] = nk[r] = 0ull;
+          ptr[r] = 0;
+          if (i < N) {
+            act |= 1u << r;
+            hk[r] = skey[(size_t)i * N];
+            if (N > 1) nk[r] = skey[(size_t)i * N + 1];
           }
-          __syncwarp();
-          for (int round = 0; round < N; round++) {
-            T bv = (T)0;
-            int brow = 0x7fffffff;
-#pragma unroll
-            for (int cc = 0; cc < KB; cc++) {
-              if (act & (1u << cc)) {
-                const T hv = hval[lane + 32 * cc];
-                if (brow == 0x7fffffff || hv > bv) { bv = hv; brow = lane + 32 * cc; }
-              }
-            }
-            if (sizeof(T) == 8) {
-              const unsigned long long b = (brow == 0x7fffffff) ? 0ull : (unsigned long long)__double_as_longlong((double)bv);
-              const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
-              const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-              const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-              brow = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)brow : 0x7fffffffu);
-            } else {
-              const unsigned b = (brow == 0x7fffffff) ? 0u : __float_as_uint((float)bv);
-              const unsigned mb = __reduce_max_sync(0xffffffffu, b);
-              brow = (int)__reduce_min_sync(0xffffffffu, b == mb ? (unsigned)brow : 0x7fffffffu);
-            }
-            const int bcol = hcol[brow];
-            if (lane == 0) mrow[brow] = bcol;
-            if ((brow & 31) == lane) act &= ~(1u << (brow >> 5));
-            if ((bcol >> 5) == lane) taken |= 1u << (bcol & 31);
-            __syncwarp();
-            // advance the rows whose head column was just taken
-#pragma unroll
-            for (int cc = 0; cc < KB; cc++) {
-              const int i = lane + 32 * cc;
-              const bool need = (act & (1u << cc)) && hcol[i] == bcol;
-              if (__any_sync(0xffffffffu, need)) {
-                int p = need ? hptr[i] : 0, col = 0;
-                bool more = need;
-                while (__any_sync(0xffffffffu, more)) {
-                  if (more) {
-                    ++p;
-                    col = ord[(size_t)i * N + p];
-                  }
-                  const uint32_t word = __shfl_sync(0xffffffffu, taken, (col >> 5) & 31);
-                  if (more && !((word >> (col & 31)) & 1u)) more = false;
-                }
-                if (need) {
-                  hptr[i] = (uint16_t)p;
-                  hcol[i] = (uint16_t)col;
-                  hval[i] = X[(size_t)i * N + col];
-                }
-              }
-            }
-            __syncwarp();
-          }
-          if (lane == 0) {  // similarity.py:150: Python sum in row order
-            double wsum = 0.0;
-            for (int i = 0; i < N; i++) wsum += (double)X[(size_t)i * N + mrow[i]];
-            s_scr[0] = wsum;
-            if (out.d) out.d[slot] = isorank_distance_of(wsum, N);
-            if (out.W) out.W[slot] = wsum;
-            if (out.iters) out.iters[slot] = it_done;
-            if (out.conv) out.conv[slot] = converged ? 1 : 0;
-          }
-          if (out.match)
-            for (int i = lane; i < N; i += 32) out.match[i] = mrow[i];
         }
+        __syncthreads();
+        for (int round = 0; round < N; round++) {
+          // local best (truncated value desc, row asc)
+          unsigned long long bv = 0ull;
+          int brow = 0x7fffffff;
+#pragma unroll
+          for (int r = 0; r < BIG_R; r++) {
+            const unsigned long long v = hk[r] >> BIG_CB;
+            if ((act >> r) & 1u) {
+              if (brow == 0x7fffffff || v > bv) { bv = v; brow = tid + BIG_THREADS * r; }
+            }
+          }
+          const bool has = brow != 0x7fffffff;
+          const unsigned hi = (unsigned)(bv >> 32), lo = (unsigned)bv;
+          const unsigned mhi = __reduce_max_sync(0xffffffffu, has ? hi : 0u);
+          const unsigned mlo = __reduce_max_sync(0xffffffffu, (has && hi == mhi) ? lo : 0u);
+          const bool cand = has && hi == mhi && lo == mlo;
+          const int wrow = (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)brow : 0x7fffffffu);
+          // rows of this warp whose head has the warp's best truncated value
+          int cnt = 0;
+#pragma unroll
+          for (int r = 0; r < BIG_R; r++)
+            cnt += ((act >> r) & 1u) && (hk[r] >> BIG_CB) == (((unsigned long long)mhi << 32) | mlo);
+          cnt = __reduce_add_sync(0xffffffffu, cnt);
+          const int buf = round & 1;
+          if (lane == 0) {
+            slot_k[buf * BIG_WARPS + warp] = wrow == 0x7fffffff ? 0ull : (((unsigned long long)mhi << 32) | mlo);
+            slot_r[buf * BIG_WARPS + warp] = wrow;
+            slot_n[buf * BIG_WARPS + warp] = wrow == 0x7fffffff ? 0 : cnt;
+          }
+          __syncthreads();
+          unsigned long long gv = 0ull;
+          int grow = 0x7fffffff, gcnt = 0;
+#pragma unroll
+          for (int w = 0; w < BIG_WARPS; w++) {
+            const unsigned long long v = slot_k[buf * BIG_WARPS + w];
+            const int rw = slot_r[buf * BIG_WARPS + w];
+            if (rw == 0x7fffffff) continue;
+            if (grow == 0x7fffffff || v > gv) { gv = v; grow = rw; gcnt = slot_n[buf * BIG_WARPS + w]; }
+            else if (v == gv) { grow = min(grow, rw); gcnt += slot_n[buf * BIG_WARPS + w]; }
+          }
+          if (shift > 0 && gcnt > 1) {
+            // several heads share the best truncated value: exact compare
+            // (X > 0, so the IEEE bits order the values)
+            unsigned long long bx = 0ull;
+            int br2 = 0x7fffffff;
+#pragma unroll
+            for (int r = 0; r < BIG_R; r++) {
+              const int i = tid + BIG_THREADS * r;
+              if (((act >> r) & 1u) && (hk[r] >> BIG_CB) == gv) {
+                const unsigned long long xb = big_bits(X[(size_t)i * N + big_key_col(hk[r])]);
+                if (br2 == 0x7fffffff || xb > bx) { bx = xb; br2 = i; }
+              }
+            }
+            const bool h2 = br2 != 0x7fffffff;
+            const unsigned x1 = (unsigned)(bx >> 32), x0 = (unsigned)bx;
+            const unsigned m1 = __reduce_max_sync(0xffffffffu, h2 ? x1 : 0u);
+            const unsigned m0 = __reduce_max_sync(0xffffffffu, (h2 && x1 == m1) ? x0 : 0u);
+            const bool c2 = h2 && x1 == m1 && x0 == m0;
+            const int r2 = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)br2 : 0x7fffffffu);
+            __syncthreads();  // slots of this buffer are read by everyone
+            if (lane == 0) {
+              slot_k[buf * BIG_WARPS + warp] = r2 == 0x7fffffff ? 0ull : (((unsigned long long)m1 << 32) | m0);
+              slot_r[buf * BIG_WARPS + warp] = r2;
+            }
+            __syncthreads();
+            gv = 0ull;
+            grow = 0x7fffffff;
+#pragma unroll
+            for (int w = 0; w < BIG_WARPS; w++) {
+              const unsigned long long v = slot_k[buf * BIG_WARPS + w];
+              const int rw = slot_r[buf * BIG_WARPS + w];
+              if (rw == 0x7fffffff) continue;
+              if (grow == 0x7fffffff || v > gv || (v == gv && rw < grow)) { gv = v; grow = rw; }
+            }
+          }
+          // winner: row grow, its head column (owner publishes it via the slot of round parity)
+          int bcol = 0;
+#pragma unroll
+          for (int r = 0; r < BIG_R; r++)
+            if (tid + BIG_THREADS * r == grow) bcol = big_key_col(hk[r]);
+          // the column is needed by everyone: broadcast through shared memory
+          int32_t *bc = slot_n + 2 * BIG_WARPS;
+          if ((grow & (BIG_THREADS - 1)) == tid) {
+            bc[buf] = bcol;
+            mrow[grow] = bcol;
+            taken[bcol >> 5] |= 1u << (bcol & 31);
+            act &= ~(1u << (grow / BIG_THREADS));
+          }
+          __syncthreads();
+          bcol = bc[buf];
+          // advance rows whose head column was taken
+#pragma unroll
+          for (int r = 0; r < BIG_R; r++) {
+            if (((act >> r) & 1u) && big_key_col(hk[r]) == bcol) {
+              const int i = tid + BIG_THREADS * r;
+              int p = ptr[r] + 1;
+              unsigned long long kk = nk[r];
+              for (;;) {
+                const int col = big_key_col(kk);
+                if (!((taken[col >> 5] >> (col & 31)) & 1u)) break;
+                ++p;  // p < N: an active row always has an untaken column
+                kk = skey[(size_t)i * N + p];
+              }
+              hk[r] = kk;
+              ptr[r] = p;
+              if (p + 1 < N) nk[r] = skey[(size_t)i * N + p + 1];
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0) {  // similarity.py:150: Python sum in row order
+          double wsum = 0.0;
+          for (int i = 0; i < N; i++) wsum += (double)X[(size_t)i * N + mrow[i]];
+          if (out.d) out.d[slot] = isorank_distance_of(wsum, N);
+          if (out.W) out.W[slot] = wsum;
+          if (out.iters) out.iters[slot] = it_done;
+          if (out.conv) out.conv[slot] = converged ? 1 : 0;
+        }
+        if (out.match)
+          for (int i = tid; i < N; i += NT) out.match[i] = mrow[i];
       }
       if (out.X)
         for (int e = tid; e < N * N; e += NT) out.X[e] = (double)X[e];

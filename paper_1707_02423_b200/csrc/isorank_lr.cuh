@@ -154,32 +154,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
     const int64_t item = *s_item;
     if (item >= work.n_items) break;
 
-    // ---- decode the work item (same scheme as the general kernel)
-    int ga, gb, ndir = 1;
+    // ---- decode the work item
+    int ga, gb, ndir;
     int64_t slot0;
-    if (work.mode == WORK_LIST) {
-      ga = work.ia[item];
-      gb = work.ib[item];
-      slot0 = work.slot ? work.slot[item] : item;
-    } else {
-      const int64_t u = work.u0 + item;
-      int lo = 0, hi = work.K - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (work.row_start[mid] <= u) lo = mid; else hi = mid - 1;
-      }
-      const int a = lo;
-      const int b = a + (int)(u - work.row_start[a]);
-      ga = work.perm[a];
-      gb = work.perm[b];
-      if (work.ordered) {
-        slot0 = 2 * (u - work.out_base);
-        ndir = (a == b) ? 1 : 2;
-      } else {
-        if (ga > gb) { const int t = ga; ga = gb; gb = t; }
-        slot0 = u - work.out_base;
-      }
-    }
+    decode_item(work, item, ga, gb, ndir, slot0);
 
     for (int dir = 0; dir < ndir; dir++) {
       const int g1 = dir ? gb : ga, g2 = dir ? ga : gb;
