@@ -208,6 +208,7 @@ int cap_for(int precision, const Plan &pl, int nlim, bool dense) {
 
 struct Scratch {
   DBuf counters, ovf_count, ovf_list, gslab, status;
+  DBuf seq_u, seq_d, seq_g, seq_n, seq_off, seq_st, seq_list, seq_apow;  // two-stage combos
   int64_t ovf_cap = 0;
 };
 
@@ -432,6 +433,180 @@ int big_status(Scratch &S, cudaStream_t st) {
     return fail(CFGSIM_ERR_CUDA, "internal: large-N kernel iteration history overflow");
   }
   return CFGSIM_OK;
+}
+
+// ---------------------------------------------------------------- two-stage small N
+// isorank_seq.cuh: per (graph, N) combo sequences (stage 1), then per-pair
+// rank-K products (stage 2).  Used for unordered all-pairs units with N <= 64
+// (CFGSIM_TWOSTAGE=0 selects the per-pair low-rank kernel instead).
+constexpr int kSeqNmax = 64;
+
+bool use_twostage() {
+  static const bool on = [] {
+    const char *e = getenv("CFGSIM_TWOSTAGE");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+template <typename T>
+int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_params *p, double *d_lin,
+                   int32_t *iters_lin, int64_t out_base, int &launch_no, cudaStream_t st) {
+  Scratch &S = scratch_for(c->device);
+  const bool f32 = sizeof(T) == 4;
+  const double tol = f32 ? std::max(p->tol, p->tol_fp32) : p->tol;
+  const int kcap = big_kcap(p->alpha, tol, p->max_iter);
+  const auto &rs = c->row_start;
+  const int a0 = (int)(std::upper_bound(rs.begin(), rs.end(), us) - rs.begin()) - 1;
+  const int a1 = (int)(std::upper_bound(rs.begin(), rs.end(), ue - 1) - rs.begin()) - 1;
+  // groups of equal N among rows a0..a1; combos (perm[b], N) for b >= first row
+  struct Grp { int N, ra, rb; int64_t cbase; };
+  std::vector<Grp> grps;
+  std::vector<int32_t> cg, cn;
+  std::vector<int64_t> uoff;
+  int64_t utot = 0;
+  for (int a = a0; a <= a1;) {
+    const int N = c->n_sorted[a];
+    int b = a;
+    while (b + 1 <= a1 && c->n_sorted[b + 1] == N) b++;
+    const int64_t base = (int64_t)cg.size();
+    grps.push_back({N, a, b, base - a});
+    for (int q = a; q < c->K; q++) {
+      cg.push_back(c->perm[q]);
+      cn.push_back(N);
+      uoff.push_back(utot);
+      utot += (int64_t)(kcap + 1) * N;
+    }
+    a = b + 1;
+  }
+  const int64_t nc = (int64_t)cg.size();
+  auto grow = [&](DBuf &b, size_t bytes) -> cudaError_t {
+    if (b.n >= bytes) return cudaSuccess;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    return b.alloc(bytes);
+  };
+  CU(grow(S.seq_u, sizeof(T) * (size_t)utot));
+  CU(grow(S.seq_d, sizeof(double) * (size_t)nc * (kcap + 1)));
+  CU(grow(S.seq_g, sizeof(int32_t) * nc));
+  CU(grow(S.seq_n, sizeof(int32_t) * nc));
+  CU(grow(S.seq_off, sizeof(int64_t) * nc));
+  CU(grow(S.seq_st, sizeof(int32_t) * nc));
+  CU(cudaMemcpyAsync(S.seq_g.p, cg.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(S.seq_n.p, cn.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(S.seq_off.p, uoff.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
+  {  // alpha^m by sequential products (the pair kernels' order)
+    std::vector<double> apow(kcap + 2);
+    apow[0] = 1.0;
+    for (int m = 1; m <= kcap + 1; m++) apow[m] = apow[m - 1] * p->alpha;
+    CU(grow(S.seq_apow, sizeof(double) * apow.size()));
+    CU(cudaMemcpyAsync(S.seq_apow.p, apow.data(), sizeof(double) * apow.size(), cudaMemcpyHostToDevice, st));
+  }
+
+  int dev, sms = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // ---- stage 1
+  SeqParams sp;
+  sp.alpha = p->alpha;
+  sp.tol = tol;
+  sp.eps = f32 ? 0.02 : 1e-6;
+  sp.max_iter = p->max_iter;
+  sp.kcap = kcap;
+  sp.nlim = kSeqNmax;
+  SeqCombos cb;
+  cb.n = nc;
+  cb.list = nullptr;
+  cb.g = S.seq_g.as<int32_t>();
+  cb.nn = S.seq_n.as<int32_t>();
+  cb.uoff = S.seq_off.as<int64_t>();
+  cb.status = S.seq_st.as<int32_t>();
+  const void *f1 = (const void *)isorank_seq_kernel<T, 2>;
+  for (int pass = 0; pass < 2; pass++) {
+    sp.cap = pass == 0 ? 14 * kSeqNmax + 16 : kSeqNmax * kSeqNmax;
+    const size_t smem = seq_smem_layout<T>(kSeqNmax, sp.cap).total;
+    CU(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f1, 128, smem));
+    if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-1 kernel cannot be resident");
+    const int64_t grid = std::min<int64_t>((int64_t)sms * occ, cb.n);
+    T *useq = S.seq_u.as<T>();
+    double *dseq = S.seq_d.as<double>();
+    DevCorpus dc = c->dev();
+    void *args[] = {(void *)&dc, (void *)&cb, (void *)&sp, (void *)&useq, (void *)&dseq};
+    CU(cudaLaunchKernel(f1, dim3((unsigned)grid), dim3(128), args, smem, st));
+    g_launches++;
+    if (pass == 1) break;
+    std::vector<int32_t> stv(nc);
+    CU(cudaMemcpyAsync(stv.data(), S.seq_st.p, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    std::vector<int64_t> redo;
+    for (int64_t q = 0; q < nc; q++)
+      if (stv[q]) redo.push_back(q);
+    if (redo.empty()) break;
+    CU(grow(S.seq_list, sizeof(int64_t) * redo.size()));
+    CU(cudaMemcpyAsync(S.seq_list.p, redo.data(), sizeof(int64_t) * redo.size(), cudaMemcpyHostToDevice, st));
+    cb.n = (int64_t)redo.size();
+    cb.list = S.seq_list.as<int64_t>();
+  }
+  // ---- stage 2: one launch per N
+  for (const Grp &gp : grps) {
+    const int64_t gu0 = std::max(us, rs[gp.ra]), gu1 = std::min(ue, rs[gp.rb + 1]);
+    if (gu1 <= gu0) continue;
+    const int N = gp.N;
+    const bool small = N <= 32;
+    const int ar = 4, bc = small ? 4 : 8, maxt = small ? 64 : 128;
+    Pair2Params pp;
+    pp.alpha = p->alpha;
+    pp.tol = tol;
+    pp.eps = f32 ? 0.02 : 1e-6;
+    pp.max_iter = p->max_iter;
+    pp.kcap = kcap;
+    pp.N = N;
+    pp.ty = (N + ar - 1) / ar;
+    pp.tx = (N + bc - 1) / bc;
+    pp.cbase = gp.cbase;
+    const int nt = std::min(maxt, std::max(64, ((pp.ty * pp.tx + 31) / 32) * 32));
+    const void *f2 = small ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 64, 8>
+                           : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 128, 4>;
+    const size_t smem = p2_smem_bytes(N, sizeof(T));
+    pp.apow = S.seq_apow.as<double>();
+    CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f2, nt, smem));
+    if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-2 kernel cannot be resident");
+    PairWork w{};
+    w.mode = WORK_TRIANGLE;
+    w.ordered = 0;
+    w.n_items = gu1 - gu0;
+    w.u0 = gu0;
+    w.out_base = out_base;
+    w.row_start = c->d_row_start.as<int64_t>();
+    w.perm = c->d_perm.as<int32_t>();
+    w.K = c->K;
+    PairOut o{};
+    o.d = d_lin;
+    o.iters = iters_lin;
+    const int64_t grid = std::min<int64_t>((int64_t)sms * occ, w.n_items);
+    unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no++ % 64);
+    CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+    const int32_t *nn = c->d_n.as<int32_t>();
+    const T *useq = S.seq_u.as<T>();
+    const double *dseq = S.seq_d.as<double>();
+    const int64_t *uo = S.seq_off.as<int64_t>();
+    void *args[] = {(void *)&nn, (void *)&w, (void *)&o, (void *)&pp, (void *)&useq, (void *)&dseq, (void *)&uo,
+                    (void *)&ctr};
+    CU(cudaLaunchKernel(f2, dim3((unsigned)grid), dim3(nt), args, smem, st));
+    g_launches++;
+  }
+  return CFGSIM_OK;
+}
+
+int seq_allpairs(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_params *p, double *d_lin,
+                 int32_t *iters_lin, int64_t out_base, int &launch_no, cudaStream_t st) {
+  if (ue <= us) return CFGSIM_OK;
+  return p->precision == CFGSIM_FP32 ? seq_allpairs_t<float>(c, us, ue, p, d_lin, iters_lin, out_base, launch_no, st)
+                                     : seq_allpairs_t<double>(c, us, ue, p, d_lin, iters_lin, out_base, launch_no, st);
 }
 
 int check_params(const cfgsim_params *p) {
@@ -981,7 +1156,20 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   o.ovf_count = S.ovf_count.as<int32_t>();
   o.ovf_list = S.ovf_list.as<int64_t>();
   o.ovf_cap = (int32_t)S.ovf_cap;
-  while (u < u1) {
+  // unordered units of rows with N <= 64 (a suffix of the size-sorted rows):
+  // two-stage path; the loop below covers the rest
+  int64_t u_end = u1;
+  const double tol_eff = p->precision == CFGSIM_FP32 ? std::max(p->tol, p->tol_fp32) : p->tol;
+  if (lr && !ordered && use_twostage() && big_kcap(p->alpha, tol_eff, p->max_iter) <= 512) {
+    int as = a;
+    while (as < c->K && c->n_sorted[as] > kSeqNmax) as++;
+    const int64_t us = std::max(u0, as < c->K ? c->row_start[as] : u1);
+    if (us < u1) {
+      if (int rc = seq_allpairs(c, us, u1, p, d_lin, iters_lin, u0, launch_no, st)) return rc;
+      u_end = us;
+    }
+  }
+  while (u < u_end) {
     const int N = c->n_sorted[a];
     int a_end = a;
     Plan pl;
@@ -1001,7 +1189,7 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
       while (a_end + 1 < c->K && plan_for(p->precision, c->n_sorted[a_end + 1], false).same_launch(pl))
         a_end++;
     }
-    const int64_t seg_end = std::min(u1, c->row_start[a_end + 1]);
+    const int64_t seg_end = std::min(u_end, c->row_start[a_end + 1]);
     w.n_items = seg_end - u;
     w.u0 = u;
     unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no % 64);

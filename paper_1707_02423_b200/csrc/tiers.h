@@ -4,6 +4,7 @@
 #include "isorank.cuh"
 #include "isorank_lr.cuh"
 #include "isorank_big.cuh"
+#include "isorank_seq.cuh"
 
 #define CFGSIM_TIER_LIST(X)      \
   X(double, 1, 4, 4, 6)          \
@@ -49,7 +50,20 @@
 // KB = sort chunks per lane: N <= 32 * KB
 #define CFGSIM_BIG_LIST_T(T, X) X(T, 8) X(T, 16) X(T, 32)
 
+// two-stage pair kernels: (T, KB, AR, BC, MAXT, MINB)
+#define CFGSIM_P2_LIST(X) \
+  X(double, 1, 4, 4, 64, 8) X(double, 2, 4, 8, 128, 4) X(float, 1, 4, 4, 64, 8) X(float, 2, 4, 8, 128, 4)
+#define CFGSIM_EXTERN_P2(T, KB, AR, BC, MAXT, MINB)                                                   \
+  extern template __global__ void cfgsim::isorank_pair2_kernel<T, KB, AR, BC, MAXT, MINB>(           \
+      const int32_t *, cfgsim::PairWork, cfgsim::PairOut, cfgsim::Pair2Params, const T *, const double *, \
+      const int64_t *, unsigned long long *);
+
 #ifndef CFGSIM_TIER_TU
+CFGSIM_P2_LIST(CFGSIM_EXTERN_P2)
+extern template __global__ void cfgsim::isorank_seq_kernel<double, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos,
+                                                                      cfgsim::SeqParams, double *, double *);
+extern template __global__ void cfgsim::isorank_seq_kernel<float, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos,
+                                                                     cfgsim::SeqParams, float *, double *);
 CFGSIM_BIG_LIST_T(double, CFGSIM_EXTERN_BIG)
 CFGSIM_BIG_LIST_T(float, CFGSIM_EXTERN_BIG)
 CFGSIM_TIER_LIST(CFGSIM_EXTERN_TIER)

@@ -298,3 +298,30 @@ def test_lowrank_and_two_product_kernels_agree(P):
     n = len(outs[0]) // 2
     np.testing.assert_array_equal(outs[0][n:], outs[1][n:])  # iteration counts
     np.testing.assert_allclose(outs[0][:n], outs[1][:n], rtol=1e-12)
+
+
+def test_two_stage_matches_per_pair_kernel(P):
+    """Two-stage all-pairs (per-(graph, N) sequences, then per-pair rank-K
+    products; isorank_seq.cuh) against the per-pair low-rank kernel
+    (CFGSIM_TWOSTAGE=0): identical iteration counts, bitwise-equal d."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "import paper_1707_02423_b200 as P; from paper_1707_02423_b200 import synth;"
+            "m = synth.random_corpus(120, 1, 64, seed=23) + [np.zeros((1, 1)), np.ones((1, 1)), np.zeros((7, 7))];"
+            "m += [np.random.default_rng(2).random((n, n)) for n in (5, 30, 64)];"
+            "t = [P.TransitionMatrix(f'g{i:03d}', x, tuple(range(len(x))), P.ROW_STOCHASTIC) for i, x in enumerate(m)];"
+            "pm, it = P.pairwise(t, P.MeasureId.ISO, return_iterations=True, precision=sys.argv[2]);"
+            "np.save(sys.argv[1], np.concatenate([pm.scores.ravel(), it.ravel().astype(float)]))")
+    for prec in ("fp64", "fp32"):
+        outs = []
+        for two in ("1", "0"):
+            path = f"/tmp/cfgsim_two_{two}_{prec}.npy"
+            env = dict(os.environ, CFGSIM_TWOSTAGE=two)
+            subprocess.run([sys.executable, "-c", code, path, prec], check=True, env=env,
+                           cwd=str(GOLDEN.parent.parent))
+            outs.append(np.load(path))
+        n = len(outs[0]) // 2
+        np.testing.assert_array_equal(outs[0][n:], outs[1][n:])
+        np.testing.assert_array_equal(outs[0][:n], outs[1][:n])
