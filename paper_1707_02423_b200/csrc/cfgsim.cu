@@ -475,7 +475,7 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
       cg.push_back(c->perm[q]);
       cn.push_back(N);
       uoff.push_back(utot);
-      utot += (int64_t)(kcap + 1) * N;
+      utot += (int64_t)(kcap + 1) * seq_pitch<T>(N);
     }
     a = b + 1;
   }
@@ -555,7 +555,7 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
     if (gu1 <= gu0) continue;
     const int N = gp.N;
     const bool small = N <= 32;
-    const int ar = 4, bc = small ? 4 : 8, maxt = small ? 64 : 128;
+    const int ar = 4, bc = small ? 4 : 8, pw = small ? 2 : 4;  // producer warps (+1 consumer warp)
     Pair2Params pp;
     pp.alpha = p->alpha;
     pp.tol = tol;
@@ -566,9 +566,15 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
     pp.ty = (N + ar - 1) / ar;
     pp.tx = (N + bc - 1) / bc;
     pp.cbase = gp.cbase;
-    const int nt = std::min(maxt, std::max(64, ((pp.ty * pp.tx + 31) / 32) * 32));
-    const void *f2 = small ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 64, 8>
-                           : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 128, 4>;
+    const int nt = 32 * (pw + 1);
+    static const int minb_env = [] {  // CFGSIM_P2_OCC=2|3: CTAs/SM the stage-2 kernel is compiled for
+      const char *e = getenv("CFGSIM_P2_OCC");
+      return e ? atoi(e) : 2;
+    }();
+    const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
+                                            : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
+                           : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
+                                            : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
     const size_t smem = p2_smem_bytes(N, sizeof(T));
     pp.apow = S.seq_apow.as<double>();
     CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

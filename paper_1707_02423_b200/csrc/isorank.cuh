@@ -745,15 +745,12 @@ __device__ double greedy_match(const T *Xs, int P, int N, uint8_t *scr, int lane
       }
     }
     __syncwarp();
-    double wsum = 0.0;  // fixed-order tree
-#pragma unroll
-    for (int cc = 0; cc < KB; cc++) {
-      const int i = lane + 32 * cc;
-      if (i < N) wsum += (double)Xs[i * P + mS[i]];
+    __syncwarp();
+    if (lane == 0) {  // similarity.py:150: Python's sum, row order
+      double wsum = 0.0;
+      for (int i = 0; i < N; i++) wsum += (double)Xs[i * P + mS[i]];
+      *wres = wsum;
     }
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, m);
-    if (lane == 0) *wres = wsum;
     if (match_out)
       for (int i = lane; i < N; i += 32) match_out[i] = mS[i];
   }

@@ -37,8 +37,9 @@ struct SeqParams {
   int32_t nlim;
 };
 
-// Combo table: combo c is graph combo_g[c] at size combo_n[c]; its u_m live
-// at useq[uoff[c] + m * combo_n[c] + t], Du_m at dseq[c * (kcap + 1) + m].
+// Combo table: combo c is graph combo_g[c] at size N = combo_n[c]; its u_m
+// live at useq[uoff[c] + m * seq_pitch<T>(N) + t] (16-byte aligned rows), Du_m
+// at dseq[c * (kcap + 1) + m].
 struct SeqCombos {
   int64_t n;
   const int64_t *list;  // NULL: combos 0..n-1, else the combo ids to build
@@ -47,6 +48,13 @@ struct SeqCombos {
   const int64_t *uoff;
   int32_t *status;  // per combo: 0 ok, 1 list overflow (re-run with dense lists)
 };
+
+// history row pitch: a multiple of 16 bytes
+template <typename T>
+__host__ __device__ inline int seq_pitch(int N) {
+  constexpr int e = 16 / (int)sizeof(T);
+  return (N + e - 1) / e * e;
+}
 
 struct SeqSmem {
   size_t dense, idx, w, toff, z, u, lo, fr, zflag, red, misc, total;
@@ -110,6 +118,7 @@ __global__ void __launch_bounds__(64 * KB) isorank_seq_kernel(DevCorpus C, SeqCo
     const int nzv = *nz;
     const T invN = (T)(1.0 / (double)N);
     T *U = useq + cb.uoff[c];
+    const int NPt = seq_pitch<T>(N);  // 16-byte aligned rows for the stage-2 copies
     double *D = dseq + c * (int64_t)(prm.kcap + 1);
     for (int t = tid; t < N; t += blockDim.x) {
       u[t] = (T)1;
@@ -124,7 +133,7 @@ __global__ void __launch_bounds__(64 * KB) isorank_seq_kernel(DevCorpus C, SeqCo
       for (int t = tid; t < N; t += blockDim.x) {
         const T v = lr_matvec_entry(toff, idx, w, zl, nzv, uo, t, invN);
         un[t] = v;
-        U[(size_t)m * N + t] = v;
+        U[(size_t)m * NPt + t] = v;
         part += fabs((double)v - (double)uo[t]);
       }
 #pragma unroll
@@ -156,53 +165,378 @@ struct Pair2Params {
   const double *apow;  // alpha^m, m = 0..kcap, by sequential products (host)
 };
 
-// Shared memory of the stage-2 kernel: X (N x P) aliased with the
-// double-buffered u/v staging, then the greedy scratch, the bracket flags.
+// Stage-2 kernel, warp-specialised: warps 0..PW-1 ("producers") compute pair
+// p's stopping sweep, X_K and row orders into one of two shared-memory
+// buffers while warp PW ("consumer") runs the greedy rounds of pair p-1 from
+// the other buffer.  Hand-off through named barriers (full / empty per
+// buffer, bar.sync / bar.arrive), so the sequential rounds overlap the GEMM
+// and sorts of the next pair.
 constexpr int P2_KC = 16;   // sweeps per staged chunk
 constexpr int P2_MW = 64;   // words of the ambiguous-sweep bitmask (kcap < 2048)
 
-__host__ __device__ inline size_t p2_x_bytes(int N, int tsize) {
-  const size_t xb = (size_t)tsize * N * (N | 1), sb = (size_t)tsize * 2 * P2_KC * 2 * N;
-  return ((xb > sb ? xb : sb) + 15) & ~(size_t)15;
-}
-__host__ __device__ inline size_t p2_smem_bytes(int N, int tsize) {
-  return p2_x_bytes(N, tsize) + (((size_t)N * N + 4 * N + 64 + 15) & ~(size_t)15) + 2 * 32 * sizeof(double) +
-         P2_MW * sizeof(uint32_t) + 64;
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-template <typename T, int KB, int AR, int BC, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB)
+struct P2Meta {
+  int64_t slot;
+  int32_t K, conv, valid, keys, emin, pad;
+};
+
+struct P2Smem {
+  size_t x[2], ord[2], meta, red, amb, item, first, mrow, total;
+};
+
+__host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize) {
+  P2Smem s;
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o += (b + 15) & ~size_t(15);
+    return at;
+  };
+  const int npt = (N + 3) & ~3, spd = ((2 * npt + 7) / 16) * 16 + 8;  // >= either T's pitch
+  size_t xb = (size_t)tsize * N * (N | 1), sb = (size_t)8 * 2 * P2_KC * spd;
+  const size_t kb = 8 * (size_t)N * (N <= 32 ? 33 : 65);  // key rows (pitch 32 KB + 1)
+  if (kb > xb) xb = kb;
+  for (int q = 0; q < 2; q++) {
+    s.x[q] = take(xb > sb ? xb : sb);  // X_K (aliases the u/v staging while it is built)
+    s.ord[q] = take((size_t)N * N);    // row orders (columns, value desc / column asc)
+  }
+  s.meta = take(2 * sizeof(P2Meta));
+  s.red = take(32 * sizeof(double));
+  s.amb = take(P2_MW * sizeof(uint32_t));
+  s.item = take(sizeof(int64_t));
+  s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
+  s.mrow = take(sizeof(int32_t) * 192);
+  s.total = o;
+  return s;
+}
+__host__ __device__ inline size_t p2_smem_bytes(int N, int tsize) { return p2_smem_layout(N, tsize).total; }
+
+// One row of X (pitch P) into ord[0..N): (value desc, column asc), the order
+// of np.argmax's first occurrence in similarity.py:103.  Exact: keys are
+// (exponent rebased on the row | mantissa | inverted column) when the row's
+// exponent span fits, else a (value, column) sort.  One warp.
+template <typename T, int KB>
+__device__ __forceinline__ void p2_sort_row(const T *row, int N, uint8_t *ord, int lane) {
+  constexpr int CB = (32 * KB <= 64) ? 6 : 7;
+  constexpr int EB = (sizeof(T) == 8) ? 12 - CB : 8;
+  T v[KB];
+  int emin = 0x7fffffff, emax = -1;
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++) {
+    const int j = lane + 32 * cc;
+    v[cc] = (j < N) ? row[j] : (T)0;
+    if (j < N) {
+      const int e = big_exponent(v[cc]);
+      emin = min(emin, e);
+      emax = max(emax, e);
+    }
+  }
+  emin = __reduce_min_sync(0xffffffffu, emin);
+  emax = __reduce_max_sync(0xffffffffu, emax);
+  if (emin > 0 && emax - emin < (1 << EB)) {
+    unsigned long long key[KB];
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int j = lane + 32 * cc;
+      unsigned long long k = 0ull;  // padding sorts last (real column fields are >= 1)
+      if (j < N) {
+        if (sizeof(T) == 8) {
+          const unsigned long long b = (unsigned long long)__double_as_longlong((double)v[cc]);
+          const unsigned long long e = ((b >> 52) & 0x7ff) - (unsigned long long)emin;
+          k = (e << (52 + CB)) | ((b & ((1ull << 52) - 1)) << CB) | (unsigned long long)((1 << CB) - 1 - j);
+        } else {
+          const unsigned int b = __float_as_uint((float)v[cc]);
+          const unsigned long long e = ((b >> 23) & 0xff) - (unsigned)emin;
+          k = (e << (23 + CB)) | ((unsigned long long)(b & 0x7fffff) << CB) | (unsigned long long)((1 << CB) - 1 - j);
+        }
+      }
+      key[cc] = k;
+    }
+    warp_sort_keys_desc<KB>(key, lane);
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int pos = lane + 32 * cc;
+      if (pos < N) ord[pos] = (uint8_t)((1 << CB) - 1 - (int)(key[cc] & ((1ull << CB) - 1)));
+    }
+  } else {
+    int cidx[KB];
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int j = lane + 32 * cc;
+      cidx[cc] = j;
+      if (j >= N) v[cc] = (T)-1;
+    }
+    warp_sort_desc<T, KB>(v, cidx, lane);
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const int pos = lane + 32 * cc;
+      if (pos < N) ord[pos] = (uint8_t)cidx[cc];
+    }
+  }
+}
+
+// Greedy rounds (similarity.py:96-108) on sorted rows, one warp: each round
+// takes the best current head over active rows (ties -> lowest row) and
+// advances the rows whose head column was taken.  Returns W (:150) on lane 0
+// (row-order sum), mrow[i] = matched column.
+template <typename T, int KB>
+__device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uint8_t *ord, int32_t *mrow, int lane) {
+  int ptr[KB], ccol[KB];
+  T cur[KB];
+  bool act[KB];
+  uint32_t taken[KB];
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++) {
+    const int i = lane + 32 * cc;
+    act[cc] = i < N;
+    ptr[cc] = 0;
+    taken[cc] = 0u;
+    ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
+    cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
+  }
+  for (int round = 0; round < N; round++) {
+    T bv = (T)0;
+    int brow = 0x7fffffff;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++)
+      if (act[cc] && (brow == 0x7fffffff || cur[cc] > bv)) { bv = cur[cc]; brow = lane + 32 * cc; }
+    const unsigned long long b = (brow == 0x7fffffff) ? 0ull : big_bits(bv);  // X > 0: bits order values
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    brow = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)brow : 0x7fffffffu);
+    int mycol = 0;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++)
+      if (cc == (brow >> 5)) mycol = ccol[cc];
+    const int bcol = __shfl_sync(0xffffffffu, mycol, brow & 31);
+    if (lane == 0) mrow[brow] = bcol;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      if (lane + 32 * cc == brow) act[cc] = false;
+      if (cc == (bcol >> 5)) taken[cc] |= 1u << (bcol & 31);
+    }
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      if (act[cc] && ccol[cc] == bcol) {
+        const int i = lane + 32 * cc;
+        int p = ptr[cc], col;
+        bool tk;
+        do {
+          ++p;
+          col = ord[i * N + p];
+          uint32_t word = 0;
+#pragma unroll
+          for (int q = 0; q < KB; q++)
+            if (q == (col >> 5)) word = taken[q];
+          tk = (word >> (col & 31)) & 1u;
+        } while (tk);
+        ptr[cc] = p;
+        ccol[cc] = col;
+        cur[cc] = Xs[i * P + col];
+      }
+    }
+  }
+  __syncwarp();
+  double wsum = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < N; i++) wsum += (double)Xs[i * P + mrow[i]];
+  return wsum;
+}
+
+// ---- exact packed keys: (value bits | 6-bit column field), comparable across
+// rows.  fp64: (exponent - emin_pair) in 6 bits | 52-bit mantissa; needs the
+// pair's exponent span < 64 (else the value-sort path is used).  fp32: the
+// 31 value bits.  X > 0 (teleport floor), so bit order is value order.
+template <typename T>
+__device__ __forceinline__ unsigned long long p2_key(T v, int col, int emin) {
+  if (sizeof(T) == 8) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong((double)v);
+    return ((((b >> 52) & 0x7ff) - (unsigned long long)emin) << 58) | ((b & ((1ull << 52) - 1)) << 6) |
+           (unsigned long long)(63 - col);
+  } else {
+    return ((unsigned long long)__float_as_uint((float)v) << 6) | (unsigned long long)(63 - col);
+  }
+}
+template <typename T>
+__device__ __forceinline__ double p2_key_value(unsigned long long k, int emin) {
+  if (sizeof(T) == 8)
+    return __longlong_as_double((long long)((((k >> 58) + (unsigned long long)emin) << 52) | ((k >> 6) & ((1ull << 52) - 1))));
+  return (double)__uint_as_float((unsigned)(k >> 6));
+}
+
+__device__ __forceinline__ void p2_cx(unsigned long long &a, unsigned long long &b, bool desc) {
+  const bool sw = desc ? (b > a) : (a > b);
+  const unsigned long long x = sw ? b : a, y = sw ? a : b;
+  a = x;
+  b = y;
+}
+
+// Bitonic sort of 32 keys held by one thread (static register indices).
+__device__ __forceinline__ void p2_sort32(unsigned long long (&v)[32], bool desc) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        const int l = i ^ j;
+        if (l > i) p2_cx(v[i], v[l], ((i & k) == 0) == desc);
+      }
+}
+// Bitonic merge of a bitonic 32-sequence held by one thread.
+__device__ __forceinline__ void p2_merge32(unsigned long long (&v)[32], bool desc) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1)
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      const int l = i ^ j;
+      if (l > i) p2_cx(v[i], v[l], desc);
+    }
+}
+
+// Greedy rounds on sorted key rows (pitch PK), one warp: a head's cross-row
+// key swaps the column field for (63 - row), so one 64-bit max picks the best
+// head with ties to the lowest row — np.argmax's first occurrence.
+template <typename T, int KB>
+__device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, int N, int emin, int32_t *mrow,
+                                                 int lane) {
+  unsigned long long hk[KB];
+  int ptr[KB];
+  bool act[KB];
+  unsigned long long taken = 0ull;
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++) {
+    const int i = lane + 32 * cc;
+    act[cc] = i < N;
+    ptr[cc] = 0;
+    hk[cc] = act[cc] ? Kr[i * PK] : 0ull;
+  }
+  double wsum = 0.0;
+  for (int round = 0; round < N; round++) {
+    unsigned long long g = 0ull;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const unsigned long long gk = (hk[cc] & ~63ull) | (unsigned long long)(63 - (lane + 32 * cc));
+      if (act[cc] && gk > g) g = gk;
+    }
+    const unsigned ghi = __reduce_max_sync(0xffffffffu, (unsigned)(g >> 32));
+    const unsigned glo = __reduce_max_sync(0xffffffffu, (unsigned)(g >> 32) == ghi ? (unsigned)g : 0u);
+    const int brow = 63 - (int)(glo & 63u);
+    unsigned long long mine = hk[0];
+#pragma unroll
+    for (int cc = 1; cc < KB; cc++)
+      if ((brow >> 5) == cc) mine = hk[cc];
+    const unsigned long long wk = __shfl_sync(0xffffffffu, mine, brow & 31);
+    const int bcol = 63 - (int)(wk & 63ull);
+    if (lane == 0) {
+      mrow[brow] = bcol;
+      mrow[64 + brow] = (int)(unsigned)(wk >> 32);  // winning key (value bits) for W
+      mrow[128 + brow] = (int)(unsigned)wk;
+    }
+    taken |= 1ull << bcol;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      if (lane + 32 * cc == brow) act[cc] = false;
+      if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
+        const int i = lane + 32 * cc;
+        int p = ptr[cc];
+        unsigned long long k;
+        do {
+          ++p;
+          k = Kr[i * PK + p];
+        } while ((taken >> (63 - (int)(k & 63ull))) & 1ull);
+        ptr[cc] = p;
+        hk[cc] = k;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0)  // similarity.py:150: Python's sum, row order
+    for (int i = 0; i < N; i++) {
+      const unsigned long long k = ((unsigned long long)(unsigned)mrow[64 + i] << 32) | (unsigned)mrow[128 + i];
+      wsum += p2_key_value<T>(k, emin);
+    }
+  return wsum;
+}
+
+template <typename T, int KB, int AR, int BC, int PW, int MINB>
+__global__ void __launch_bounds__(32 * (PW + 1), MINB)
     isorank_pair2_kernel(const int32_t *n_nodes, PairWork work, PairOut out, Pair2Params prm, const T *useq,
                          const double *dseq, const int64_t *uoff, unsigned long long *counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = prm.N, P = N | 1;
-  T *Xs = (T *)smem_raw;  // N x P (aliases the staging buffers)
-  T *stg = (T *)smem_raw;
-  uint8_t *scr = smem_raw + p2_x_bytes(N, sizeof(T));
-  double *red = (double *)(scr + ((((size_t)N * N + 4 * N + 64) + 15) & ~(size_t)15));
-  uint32_t *amb = (uint32_t *)(red + 2 * 32);
-  int64_t *s_item = (int64_t *)(amb + P2_MW);
-  int32_t *s_first = (int32_t *)(s_item + 1);
+  const P2Smem L = p2_smem_layout(N, sizeof(T));
+  P2Meta *meta = (P2Meta *)(smem_raw + L.meta);
+  double *red = (double *)(smem_raw + L.red);
+  uint32_t *amb = (uint32_t *)(smem_raw + L.amb);
+  int64_t *s_item = (int64_t *)(smem_raw + L.item);
+  int32_t *s_first = (int32_t *)(smem_raw + L.first);
+  constexpr int NP = 32 * PW;       // producer threads
+  constexpr int NALL = NP + 32;     // producers + consumer warp
+  constexpr int BAR_P = 1, BAR_FULL = 2, BAR_EMPTY = 4;  // named barriers (ids 2,3 / 4,5 per buffer)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
+  const double inv_nn = 1.0 / (double)((long long)N * N);
+
+  if (warp == PW) {
+    // ---------------- consumer: greedy rounds of the pairs in order
+    int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
+    for (int it = 0;; it++) {
+      const int s = it & 1;
+      nbar_sync(BAR_FULL + s, NALL);
+      const P2Meta mt = meta[s];
+      if (!mt.valid) break;
+      const T *Xs = (const T *)(smem_raw + L.x[s]);
+      const double wsum =
+          mt.keys ? p2_rounds_keys<T, KB>((const unsigned long long *)Xs, 32 * KB + 1, N, mt.emin, mrow, lane)
+                  : p2_rounds<T, KB>(Xs, P, N, smem_raw + L.ord[s], mrow, lane);
+      if (lane == 0) {
+        if (out.d) out.d[mt.slot] = isorank_distance_of(wsum, N);
+        if (out.W) out.W[mt.slot] = wsum;
+        if (out.iters) out.iters[mt.slot] = mt.K;
+        if (out.conv) out.conv[mt.slot] = mt.conv;
+      }
+      __syncwarp();
+      nbar_arrive(BAR_EMPTY + s, NALL);
+    }
+    return;
+  }
+
+  // ---------------- producers
   const int TY = prm.ty, TX = prm.tx;
   const bool owner = tid < TY * TX;
   const int ty = owner ? tid / TX : 0, tx = owner ? tid - (tid / TX) * TX : 0;
   const double invN = 1.0 / (double)N;
-  const double inv_nn = 1.0 / (double)((long long)N * N);
   const double c = (1.0 - prm.alpha) * inv_nn;
   const int mmax = prm.max_iter < prm.kcap ? prm.max_iter : prm.kcap;
-
-  for (;;) {
+  const int NPt = seq_pitch<T>(N);                      // history row pitch
+  const int SPD = ((2 * NPt + 7) / 16) * 16 + 8;        // staged row pitch (== 8 mod 16 doubles: 2-wavefront fragments)
+  for (int it = 0;; it++) {
+    const int s = it & 1;
     if (tid == 0) {
       *s_item = (int64_t)atomicAdd(counter, 1ull);
-      *s_first = 0x7fffffff;
+      s_first[0] = 0x7fffffff;
+      s_first[1] = 0x7fffffff;
+      s_first[2] = -1;
     }
-    for (int q = tid; q < P2_MW; q += NT) amb[q] = 0u;
-    __syncthreads();
+    for (int q = tid; q < P2_MW; q += NP) amb[q] = 0u;
+    nbar_sync(BAR_P, NP);
     const int64_t item = *s_item;
-    if (item >= work.n_items) break;
+    if (it >= 2) nbar_sync(BAR_EMPTY + s, NALL);  // buffer s released by the consumer (pair it-2)
+    if (item >= work.n_items) {
+      if (tid == 0) meta[s].valid = 0;
+      nbar_arrive(BAR_FULL + s, NALL);
+      if (it >= 1) nbar_sync(BAR_EMPTY + (s ^ 1), NALL);  // match the consumer's last release
+      break;
+    }
+    T *Xs = (T *)(smem_raw + L.x[s]);
+    T *stg = Xs;
+    uint8_t *ord = smem_raw + L.ord[s];
     // triangle unit -> sorted rows a <= b; the alignment runs in the caller's
     // (lower graph index, higher graph index) direction
     const int64_t uu = work.u0 + item;
@@ -225,7 +559,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     // parallel (alpha^m from the host's table, the same sequential products),
     // then exact delta only for the ambiguous sweeps before the first
     // certain stop, in order
-    for (int m = tid + 1; m <= mmax; m += NT) {
+    for (int m = tid + 1; m <= mmax; m += NP) {
       const double ak = prm.apow[m];
       const double da = DA[m], db = DB[m];
       const double hiB = ak * invN * (da + db) * (1.0 + prm.eps);
@@ -233,13 +567,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (hiB < prm.tol) atomicMin(s_first, m);
       else if (loB < prm.tol) atomicOr(amb + (m >> 5), 1u << (m & 31));
     }
-    __syncthreads();
+    nbar_sync(BAR_P, NP);
     int K = mmax;
     bool conv = false;
     {
       const int first = *s_first;
       if (first != 0x7fffffff) { K = first; conv = true; }
-      const int lim = first == 0x7fffffff ? mmax : first - 1;  // ambiguous sweeps that can still decide
+      const int lim = first == 0x7fffffff ? mmax : first - 1;
       for (int wd = 0; wd <= (lim >> 5); wd++) {
         uint32_t bits = amb[wd];
         while (bits) {
@@ -247,20 +581,20 @@ __global__ void __launch_bounds__(MAXT, MINB)
           bits &= bits - 1;
           if (m > lim) break;
           // exact delta_m = alpha^m/N^2 sum_ij |u_m[i] v_m[j] - u_{m-1}[i] v_{m-1}[j]|
-          const T *un = UA + (size_t)m * N, *uo = UA + (size_t)(m - 1) * N;
-          const T *vn = UB + (size_t)m * N, *vo = UB + (size_t)(m - 1) * N;
+          const T *un = UA + (size_t)m * NPt, *uo = UA + (size_t)(m - 1) * NPt;
+          const T *vn = UB + (size_t)m * NPt, *vo = UB + (size_t)(m - 1) * NPt;
           double dl = 0.0;
-          for (int e = tid; e < N * N; e += NT) {
+          for (int e = tid; e < N * N; e += NP) {
             const int i = e / N, j = e - (e / N) * N;
             dl += fabs((double)fma(-uo[i], vo[j], un[i] * vn[j]));
           }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) dl += __shfl_xor_sync(0xffffffffu, dl, o);
           if (lane == 0) red[warp] = dl;
-          __syncthreads();
+          nbar_sync(BAR_P, NP);
           double S = 0.0;
-          for (int q = 0; q < NW; q++) S += red[q];
-          __syncthreads();  // red is rewritten by the next exact pass
+          for (int q = 0; q < PW; q++) S += red[q];
+          nbar_sync(BAR_P, NP);  // red is rewritten by the next exact pass
           if (prm.apow[m] * inv_nn * S < prm.tol) {  // similarity.py:144
             K = m;
             conv = true;
@@ -273,88 +607,246 @@ __global__ void __launch_bounds__(MAXT, MINB)
 
     // ---- X_K = sum_{m<K} (c alpha^m) u_m v_m^T + (alpha^K/N^2) u_K v_K^T, the
     // u/v rows staged through shared memory in chunks of P2_KC sweeps
-    T Pacc[AR][BC];
-#pragma unroll
-    for (int x = 0; x < AR; x++)
-#pragma unroll
-      for (int y = 0; y < BC; y++) Pacc[x][y] = 0;
+    // (16-byte cp.async; rows past K zero-filled up to the chunk's end)
     const int nch = (K + 1 + P2_KC - 1) / P2_KC;  // rows m = 0..K
     auto stage = [&](int ch) {
-      T *dst = stg + (ch & 1) * P2_KC * 2 * N;
+      T *dst = stg + (ch & 1) * P2_KC * SPD;
       const int m0 = ch * P2_KC;
-      const int rows = (K + 1 - m0) < P2_KC ? (K + 1 - m0) : P2_KC;
-      for (int e = tid; e < rows * 2 * N; e += NT) {
-        const int mm = e / (2 * N), r = e - mm * 2 * N;
-        const T *src = (r < N ? UA + (size_t)(m0 + mm) * N + r : UB + (size_t)(m0 + mm) * N + (r - N));
-        big_cp_async_zfill<sizeof(T)>(dst + e, src, true);
+      constexpr int EPU = 16 / sizeof(T);  // elements per 16-byte copy
+      const int upr = NPt / EPU;           // copies per u (or v) row
+      for (int mm = 0; mm < P2_KC; mm++) {
+        const bool ok = m0 + mm <= K;
+        for (int q = tid; q < 2 * upr; q += NP) {
+          const int side = q >= upr, r = (q - side * upr) * EPU;
+          const T *src = (side ? UB : UA) + (size_t)(ok ? m0 + mm : 0) * NPt + r;
+          big_cp_async_zfill<16>(dst + mm * SPD + side * NPt + r, src, ok);
+        }
       }
       big_cp_async_commit();
     };
     stage(0);
-    int ii[AR], jj[BC];
+    int emn = 0x7fffffff, emx = -1;
+    if constexpr (sizeof(T) == 8) {
+      // fp64 tensor cores: mma.m8n8k4 accumulates each 8x8 tile as the fma
+      // chain over k in order (bitwise equal to the scalar chain, probed on
+      // B200: tools/probes/dmma_probe.cu), so X is the same as the m-ascending
+      // fma accumulation of the low-rank kernel.  Warp tile grid WR x WC,
+      // TR x TC 8x8 tiles per warp.
+      constexpr int WR = 2, WC = PW / 2, TR = (KB == 1) ? 2 : 4, TC = 4;
+      const int wr = warp % WR, wc = warp / WR;
+      const int lr = lane >> 2, lk = lane & 3;
+      double acc[TR][TC][2];
 #pragma unroll
-    for (int x = 0; x < AR; x++) { ii[x] = ty + TY * x; if (ii[x] >= N) ii[x] = N - 1; }
+      for (int x = 0; x < TR; x++)
 #pragma unroll
-    for (int y = 0; y < BC; y++) { jj[y] = tx + TX * y; if (jj[y] >= N) jj[y] = N - 1; }
-    T uK[AR], vK[BC];
-    for (int ch = 0; ch < nch; ch++) {
-      if (ch + 1 < nch) {
-        stage(ch + 1);
-        big_cp_async_wait_group<1>();
-      } else {
-        big_cp_async_wait_group<0>();
+        for (int y = 0; y < TC; y++) acc[x][y][0] = acc[x][y][1] = 0.0;
+      for (int ch = 0; ch < nch; ch++) {
+        if (ch + 1 < nch) {
+          stage(ch + 1);
+          big_cp_async_wait_group<1>();
+        } else {
+          big_cp_async_wait_group<0>();
+        }
+        nbar_sync(BAR_P, NP);
+        const double *buf = (const double *)stg + (ch & 1) * P2_KC * SPD;
+        const int m0 = ch * P2_KC;
+#pragma unroll
+        for (int k0 = 0; k0 < P2_KC; k0 += 4) {
+          const int m = m0 + k0 + lk;  // this lane's k
+          if (m0 + k0 > K) break;
+          const double cf = (m < K) ? (double)(T)(c * prm.apow[m]) : (m == K ? (double)(T)(prm.apow[K] * inv_nn) : 0.0);
+          const double *row = buf + (k0 + lk) * SPD;
+          double af[TR], bf[TC];
+#pragma unroll
+          for (int x = 0; x < TR; x++) {
+            const int i = (wr * TR + x) * 8 + lr;
+            af[x] = cf * (i < N ? row[i] : 0.0);
+          }
+#pragma unroll
+          for (int y = 0; y < TC; y++) {
+            const int j = (wc * TC + y) * 8 + lr;
+            bf[y] = j < N ? row[NPt + j] : 0.0;
+          }
+#pragma unroll
+          for (int x = 0; x < TR; x++)
+#pragma unroll
+            for (int y = 0; y < TC; y++)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                           : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                           : "d"(af[x]), "d"(bf[y]));
+        }
+        nbar_sync(BAR_P, NP);  // buffer (ch & 1) is re-staged by chunk ch + 2 / keys overwrite it
       }
-      __syncthreads();
-      const T *buf = stg + (ch & 1) * P2_KC * 2 * N;
-      const int m0 = ch * P2_KC;
-      const int rows = (K + 1 - m0) < P2_KC ? (K + 1 - m0) : P2_KC;
+#pragma unroll
+      for (int x = 0; x < TR; x++)
+#pragma unroll
+        for (int y = 0; y < TC; y++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int i = (wr * TR + x) * 8 + lr, j = (wc * TC + y) * 8 + 2 * lk + h;
+            if (i < N && j < N) {
+              const int e = big_exponent(acc[x][y][h]);
+              emn = min(emn, e);
+              emx = max(emx, e);
+            }
+          }
+      emn = __reduce_min_sync(0xffffffffu, emn);
+      emx = __reduce_max_sync(0xffffffffu, emx);
+      if (lane == 0) {
+        atomicMin(s_first + 1, emn);
+        atomicMax(s_first + 2, emx);
+      }
+      nbar_sync(BAR_P, NP);
+      const int emin = s_first[1];
+      const bool keys = s_first[2] - emin < 64;
+      constexpr int PK = 32 * KB + 1;
+      unsigned long long *Kr = (unsigned long long *)Xs;
+#pragma unroll
+      for (int x = 0; x < TR; x++)
+#pragma unroll
+        for (int y = 0; y < TC; y++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int i = (wr * TR + x) * 8 + lr, j = (wc * TC + y) * 8 + 2 * lk + h;
+            if (i < N && j < N) {
+              if (keys) Kr[i * PK + j] = p2_key<T>((T)acc[x][y][h], j, emin);
+              else Xs[i * P + j] = (T)acc[x][y][h];
+            }
+          }
+    } else {
+      T Pacc[AR][BC];
+#pragma unroll
+      for (int x = 0; x < AR; x++)
+#pragma unroll
+        for (int y = 0; y < BC; y++) Pacc[x][y] = 0;
+      int ii[AR], jj[BC];
+#pragma unroll
+      for (int x = 0; x < AR; x++) { ii[x] = ty + TY * x; if (ii[x] >= N) ii[x] = N - 1; }
+#pragma unroll
+      for (int y = 0; y < BC; y++) { jj[y] = tx + TX * y; if (jj[y] >= N) jj[y] = N - 1; }
+      T uK[AR], vK[BC];
+      for (int ch = 0; ch < nch; ch++) {
+        if (ch + 1 < nch) {
+          stage(ch + 1);
+          big_cp_async_wait_group<1>();
+        } else {
+          big_cp_async_wait_group<0>();
+        }
+        nbar_sync(BAR_P, NP);
+        const T *buf = stg + (ch & 1) * P2_KC * SPD;
+        const int m0 = ch * P2_KC;
+        const int rows = (K + 1 - m0) < P2_KC ? (K + 1 - m0) : P2_KC;
+        if (owner) {
+          for (int mm = 0; mm < rows; mm++) {
+            const int m = m0 + mm;
+            const T *um = buf + mm * SPD, *vm = um + NPt;
+            if (m == K) {  // last term
+#pragma unroll
+              for (int x = 0; x < AR; x++) uK[x] = um[ii[x]];
+#pragma unroll
+              for (int y = 0; y < BC; y++) vK[y] = vm[jj[y]];
+              break;
+            }
+            const T cak = (T)(c * prm.apow[m]);
+            T vb[BC];
+#pragma unroll
+            for (int y = 0; y < BC; y++) vb[y] = vm[jj[y]];
+#pragma unroll
+            for (int x = 0; x < AR; x++) {
+              const T cu = cak * um[ii[x]];
+#pragma unroll
+              for (int y = 0; y < BC; y++) Pacc[x][y] = fma(cu, vb[y], Pacc[x][y]);
+            }
+          }
+        }
+        nbar_sync(BAR_P, NP);  // buffer (ch & 1) is re-staged by chunk ch + 2 / X overwrites it
+      }
       if (owner) {
-        for (int mm = 0; mm < rows; mm++) {
-          const int m = m0 + mm;
-          const T *um = buf + mm * 2 * N, *vm = um + N;
-          if (m == K) {  // last term
+        const T sc = (T)(prm.apow[K] * inv_nn);
 #pragma unroll
-            for (int x = 0; x < AR; x++) uK[x] = um[ii[x]];
+        for (int x = 0; x < AR; x++) {
+          const T su = sc * uK[x];
 #pragma unroll
-            for (int y = 0; y < BC; y++) vK[y] = vm[jj[y]];
-            break;
+          for (int y = 0; y < BC; y++) {
+            Pacc[x][y] = fma(su, vK[y], Pacc[x][y]);
+            if (ty + TY * x < N && tx + TX * y < N) {
+              const int e = big_exponent(Pacc[x][y]);
+              emn = min(emn, e);
+              emx = max(emx, e);
+            }
           }
-          const T cak = (T)(c * prm.apow[m]);
-          T vb[BC];
+        }
+        emn = __reduce_min_sync(__activemask(), emn);
+        emx = __reduce_max_sync(__activemask(), emx);
+        if (lane == 0 || !(__activemask() & ((1u << lane) - 1))) {
+          atomicMin(s_first + 1, emn);
+          atomicMax(s_first + 2, emx);
+        }
+      }
+      nbar_sync(BAR_P, NP);
+      const int emin = s_first[1];
+      constexpr int PK = 32 * KB + 1;
+      unsigned long long *Kr = (unsigned long long *)Xs;
+      if (owner) {
 #pragma unroll
-          for (int y = 0; y < BC; y++) vb[y] = vm[jj[y]];
+        for (int x = 0; x < AR; x++) {
+          const int i = ty + TY * x;
 #pragma unroll
-          for (int x = 0; x < AR; x++) {
-            const T cu = cak * um[ii[x]];
-#pragma unroll
-            for (int y = 0; y < BC; y++) Pacc[x][y] = fma(cu, vb[y], Pacc[x][y]);
+          for (int y = 0; y < BC; y++) {
+            const int j = tx + TX * y;
+            if (i < N && j < N) Kr[i * PK + j] = p2_key<T>(Pacc[x][y], j, emin);
           }
         }
       }
-      __syncthreads();  // buffer (ch & 1) is re-staged by chunk ch + 2 / X overwrites it
     }
-    if (owner) {
-      const T sc = (T)(prm.apow[K] * inv_nn);
+    nbar_sync(BAR_P, NP);
+    const int emin = s_first[1];
+    const bool keys = sizeof(T) == 4 || (s_first[2] - emin < 64);
+    constexpr int PK = 32 * KB + 1;
+    unsigned long long *Kr = (unsigned long long *)Xs;
+    if (keys) {
+      // ---- row orders: one thread per row (N <= 32) or per half row with a
+      // cross-thread bitonic merge (N <= 64), 32 keys in registers
+      const int row = (KB == 1) ? tid : (tid & 63), half = (KB == 1) ? 0 : (tid >> 6);
+      const bool act = row < N && (KB == 1 ? tid < 32 : tid < 128);
+      unsigned long long v[32];
+      if (act) {
 #pragma unroll
-      for (int x = 0; x < AR; x++) {
-        const int i = ty + TY * x;
-        const T su = sc * uK[x];
-#pragma unroll
-        for (int y = 0; y < BC; y++) {
-          const int j = tx + TX * y;
-          if (i < N && j < N) Xs[i * P + j] = fma(su, vK[y], Pacc[x][y]);
+        for (int q = 0; q < 32; q++) {
+          const int j = half * 32 + q;
+          v[q] = (j < N) ? Kr[row * PK + j] : 0ull;  // padding sorts last
         }
+        p2_sort32(v, half == 0);
       }
+      if (KB == 2) {
+        if (act)
+#pragma unroll
+          for (int q = 0; q < 32; q++) Kr[row * PK + half * 32 + q] = v[q];
+        nbar_sync(BAR_P, NP);
+        if (act)
+#pragma unroll
+          for (int q = 0; q < 32; q++) {  // half 0 keeps the larger 32, half 1 the smaller
+            const unsigned long long o = Kr[row * PK + (half ^ 1) * 32 + q];
+            v[q] = (half == 0) ? (o > v[q] ? o : v[q]) : (o > v[q] ? v[q] : o);
+          }
+        nbar_sync(BAR_P, NP);
+        if (act) p2_merge32(v, true);
+      }
+      if (act)
+#pragma unroll
+        for (int q = 0; q < 32; q++) Kr[row * PK + half * 32 + q] = v[q];
+    } else {
+      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * N, lane);
     }
-    __syncthreads();
-    const double wsum = greedy_match<T, KB>(Xs, P, N, scr, lane, warp, NW, nullptr);
     if (tid == 0) {
-      if (out.d) out.d[slot] = isorank_distance_of(wsum, N);
-      if (out.W) out.W[slot] = wsum;
-      if (out.iters) out.iters[slot] = K;
-      if (out.conv) out.conv[slot] = conv ? 1 : 0;
+      meta[s].slot = slot;
+      meta[s].K = K;
+      meta[s].conv = conv ? 1 : 0;
+      meta[s].valid = 1;
+      meta[s].keys = keys ? 1 : 0;
+      meta[s].emin = emin;
     }
-    __syncthreads();
+    nbar_arrive(BAR_FULL + s, NALL);  // publishes X, ord, meta (bar.arrive orders prior smem writes)
   }
 }
 
