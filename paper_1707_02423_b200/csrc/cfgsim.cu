@@ -569,7 +569,7 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
     const int nt = 32 * (pw + 1);
     static const int minb_env = [] {  // CFGSIM_P2_OCC=2|3: CTAs/SM the stage-2 kernel is compiled for
       const char *e = getenv("CFGSIM_P2_OCC");
-      return e ? atoi(e) : 2;
+      return e ? atoi(e) : 3;
     }();
     const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
                                             : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)

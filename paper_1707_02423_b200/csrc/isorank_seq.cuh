@@ -399,12 +399,65 @@ __device__ __forceinline__ void p2_merge32(unsigned long long (&v)[32], bool des
     }
 }
 
+// Bitonic sort (descending) of n = 32 KB 32-bit keys held by one thread.
+template <int KB>
+__device__ __forceinline__ void p2_sort_u32(uint32_t (&v)[32 * KB]) {
+  constexpr int n = 32 * KB;
+#pragma unroll
+  for (int k = 2; k <= n; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < n; i++) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t a = v[i], b = v[l];
+          const uint32_t hi = max(a, b), lo = min(a, b);
+          if ((i & k) == 0) { v[i] = hi; v[l] = lo; } else { v[i] = lo; v[l] = hi; }
+        }
+      }
+}
+
+// One row's order by one thread: 32-bit keys (top 26 value bits | column
+// field) sorted in registers; adjacent entries whose 26-bit prefixes tie but
+// whose exact keys differ are re-ordered by an insertion pass on the exact
+// 64-bit keys (rare: near-ties within ~1e-6 relative).
+template <typename T, int KB>
+__device__ __forceinline__ void p2_row_order(const unsigned long long *Krow, int N, uint8_t *ord) {
+  constexpr int VB = sizeof(T) == 8 ? 58 : 31;  // value bits above the column field
+  uint32_t v[32 * KB];
+#pragma unroll
+  for (int q = 0; q < 32 * KB; q++)
+    v[q] = (q < N) ? (uint32_t)((((Krow[q] >> 6) >> (VB - 26)) << 6) | (Krow[q] & 63ull)) : 0u;  // padding last
+  p2_sort_u32<KB>(v);
+  bool coll = false;
+#pragma unroll
+  for (int q = 0; q < 32 * KB; q++) {
+    if (q < N) ord[q] = (uint8_t)(63 - (int)(v[q] & 63u));
+    if (q + 1 < 32 * KB && q + 1 < N && (v[q] >> 6) == (v[q + 1] >> 6) &&
+        (Krow[63 - (v[q] & 63u)] >> 6) != (Krow[63 - (v[q + 1] & 63u)] >> 6))
+      coll = true;
+  }
+  if (coll) {
+    for (int p = 1; p < N; p++) {
+      const uint8_t cp = ord[p];
+      const unsigned long long kp = Krow[cp];
+      int q = p - 1;
+      while (q >= 0 && Krow[ord[q]] < kp) {  // exact key order: value desc, column asc
+        ord[q + 1] = ord[q];
+        q--;
+      }
+      ord[q + 1] = cp;
+    }
+  }
+}
+
 // Greedy rounds on sorted key rows (pitch PK), one warp: a head's cross-row
 // key swaps the column field for (63 - row), so one 64-bit max picks the best
 // head with ties to the lowest row — np.argmax's first occurrence.
 template <typename T, int KB>
-__device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, int N, int emin, int32_t *mrow,
-                                                 int lane) {
+__device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, const uint8_t *ord, int N, int emin,
+                                                 int32_t *mrow, int lane) {
   unsigned long long hk[KB];
   int ptr[KB];
   bool act[KB];
@@ -414,7 +467,7 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
     const int i = lane + 32 * cc;
     act[cc] = i < N;
     ptr[cc] = 0;
-    hk[cc] = act[cc] ? Kr[i * PK] : 0ull;
+    hk[cc] = act[cc] ? Kr[i * PK + ord[i * N]] : 0ull;
   }
   double wsum = 0.0;
   for (int round = 0; round < N; round++) {
@@ -444,14 +497,13 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
       if (lane + 32 * cc == brow) act[cc] = false;
       if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
         const int i = lane + 32 * cc;
-        int p = ptr[cc];
-        unsigned long long k;
+        int p = ptr[cc], col;
         do {
           ++p;
-          k = Kr[i * PK + p];
-        } while ((taken >> (63 - (int)(k & 63ull))) & 1ull);
+          col = ord[i * N + p];
+        } while ((taken >> col) & 1ull);
         ptr[cc] = p;
-        hk[cc] = k;
+        hk[cc] = Kr[i * PK + col];
       }
     }
   }
@@ -493,7 +545,8 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       if (!mt.valid) break;
       const T *Xs = (const T *)(smem_raw + L.x[s]);
       const double wsum =
-          mt.keys ? p2_rounds_keys<T, KB>((const unsigned long long *)Xs, 32 * KB + 1, N, mt.emin, mrow, lane)
+          mt.keys ? p2_rounds_keys<T, KB>((const unsigned long long *)Xs, 32 * KB + 1, smem_raw + L.ord[s], N, mt.emin,
+                                          mrow, lane)
                   : p2_rounds<T, KB>(Xs, P, N, smem_raw + L.ord[s], mrow, lane);
       if (lane == 0) {
         if (out.d) out.d[mt.slot] = isorank_distance_of(wsum, N);
@@ -805,36 +858,8 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     constexpr int PK = 32 * KB + 1;
     unsigned long long *Kr = (unsigned long long *)Xs;
     if (keys) {
-      // ---- row orders: one thread per row (N <= 32) or per half row with a
-      // cross-thread bitonic merge (N <= 64), 32 keys in registers
-      const int row = (KB == 1) ? tid : (tid & 63), half = (KB == 1) ? 0 : (tid >> 6);
-      const bool act = row < N && (KB == 1 ? tid < 32 : tid < 128);
-      unsigned long long v[32];
-      if (act) {
-#pragma unroll
-        for (int q = 0; q < 32; q++) {
-          const int j = half * 32 + q;
-          v[q] = (j < N) ? Kr[row * PK + j] : 0ull;  // padding sorts last
-        }
-        p2_sort32(v, half == 0);
-      }
-      if (KB == 2) {
-        if (act)
-#pragma unroll
-          for (int q = 0; q < 32; q++) Kr[row * PK + half * 32 + q] = v[q];
-        nbar_sync(BAR_P, NP);
-        if (act)
-#pragma unroll
-          for (int q = 0; q < 32; q++) {  // half 0 keeps the larger 32, half 1 the smaller
-            const unsigned long long o = Kr[row * PK + (half ^ 1) * 32 + q];
-            v[q] = (half == 0) ? (o > v[q] ? o : v[q]) : (o > v[q] ? v[q] : o);
-          }
-        nbar_sync(BAR_P, NP);
-        if (act) p2_merge32(v, true);
-      }
-      if (act)
-#pragma unroll
-        for (int q = 0; q < 32; q++) Kr[row * PK + half * 32 + q] = v[q];
+      // ---- row orders: one thread per row, 32-bit prefix keys in registers
+      if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * N);
     } else {
       for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * N, lane);
     }
