@@ -171,7 +171,7 @@ struct Pair2Params {
 // the other buffer.  Hand-off through named barriers (full / empty per
 // buffer, bar.sync / bar.arrive), so the sequential rounds overlap the GEMM
 // and sorts of the next pair.
-constexpr int P2_KC = 16;   // sweeps per staged chunk
+constexpr int P2_KC = 8;    // sweeps per staged chunk
 constexpr int P2_MW = 64;   // words of the ambiguous-sweep bitmask (kcap < 2048)
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
@@ -662,19 +662,20 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     // u/v rows staged through shared memory in chunks of P2_KC sweeps
     // (16-byte cp.async; rows past K zero-filled up to the chunk's end)
     const int nch = (K + 1 + P2_KC - 1) / P2_KC;  // rows m = 0..K
+    // staging assignment: copy q (16 bytes) of rows mm0, mm0 + sstep, ...
+    constexpr int EPU = 16 / sizeof(T);  // elements per 16-byte copy
+    const int upr = NPt / EPU, w2 = 2 * upr;
+    const int sstep = NP / w2, sq = tid % w2, smm0 = tid / w2;
+    const int sside = sq >= upr, sr = (sq - sside * upr) * EPU;
+    const T *ssrc = (sside ? UB : UA) + sr;
     auto stage = [&](int ch) {
-      T *dst = stg + (ch & 1) * P2_KC * SPD;
+      T *dst = stg + (ch & 1) * P2_KC * SPD + sside * NPt + sr;
       const int m0 = ch * P2_KC;
-      constexpr int EPU = 16 / sizeof(T);  // elements per 16-byte copy
-      const int upr = NPt / EPU;           // copies per u (or v) row
-      for (int mm = 0; mm < P2_KC; mm++) {
-        const bool ok = m0 + mm <= K;
-        for (int q = tid; q < 2 * upr; q += NP) {
-          const int side = q >= upr, r = (q - side * upr) * EPU;
-          const T *src = (side ? UB : UA) + (size_t)(ok ? m0 + mm : 0) * NPt + r;
-          big_cp_async_zfill<16>(dst + mm * SPD + side * NPt + r, src, ok);
+      if (smm0 < sstep)
+        for (int mm = smm0; mm < P2_KC; mm += sstep) {
+          const bool ok = m0 + mm <= K;
+          big_cp_async_zfill<16>(dst + mm * SPD, ssrc + (size_t)(ok ? m0 + mm : 0) * NPt, ok);
         }
-      }
       big_cp_async_commit();
     };
     stage(0);
