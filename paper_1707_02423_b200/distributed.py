@@ -112,3 +112,41 @@ def gpu_compute_range(corpus, params, stream=None):
         return out[: u1 - u0].cpu().numpy()
 
     return run
+
+
+def merge_best(d, idx):
+    """Lexicographic (d, index) minimum over shards: d, idx are [world, nq]
+    tensors (or arrays) of per-shard best matches; returns (best_d, best_idx)
+    — np.argmin's lowest-index tie rule over the concatenated corpus."""
+    import torch
+
+    d = torch.as_tensor(d)
+    idx = torch.as_tensor(idx)
+    best = d.min(dim=0).values
+    cand = torch.where(d == best.unsqueeze(0), idx, torch.full_like(idx, torch.iinfo(idx.dtype).max))
+    return best, cand.min(dim=0).values
+
+
+def nearest_sharded(n_corpus: int, compute_shard: Callable[[int, int], tuple], *, group=None, device=None):
+    """Query-vs-corpus best match with the corpus split into world shards
+    (SURVEY §8(e)): ``compute_shard(c0, c1) -> (best_d[nq], best_idx[nq])``
+    on this rank's shard, then one all-gather of the candidates and the
+    lexicographic (d, index) minimum on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    bounds = np.linspace(0, n_corpus, world + 1).astype(np.int64)
+    bd, bi = compute_shard(int(bounds[rank]), int(bounds[rank + 1]))
+    dev = device if device is not None else torch.device("cpu")
+    td = torch.as_tensor(np.asarray(bd, np.float64), device=dev)
+    ti = torch.as_tensor(np.asarray(bi, np.int64), device=dev)
+    if world == 1:
+        return td.cpu().numpy(), ti.cpu().numpy()
+    gd = torch.empty(world * len(td), dtype=torch.float64, device=dev)
+    gi = torch.empty(world * len(ti), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(gd, td, group=group)
+    dist.all_gather_into_tensor(gi, ti, group=group)
+    best, idx = merge_best(gd.view(world, -1), gi.view(world, -1))
+    return best.cpu().numpy(), idx.cpu().numpy()

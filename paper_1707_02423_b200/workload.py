@@ -63,3 +63,11 @@ def triangle_units(n_nodes: np.ndarray):
     row_start = np.concatenate([[0], np.cumsum(np.arange(k, 0, -1))])
     b = a + (np.arange(len(a)) - row_start[a])
     return perm, a, b
+
+
+def side_stats(m, N: int) -> tuple[int, int]:
+    """(S, z) of one graph at common size N: nonzeros outside uniform rows and
+    the number of uniform (all-zero) rows of interpolate_to(m, N)."""
+    e = np.asarray(getattr(m, "entries", m), float)
+    a = _interp_pattern(e, N) != 0
+    return int(a.sum()), int((~a.any(axis=1)).sum())

@@ -96,3 +96,66 @@ def test_gloo_world2_matches_single_rank(tmp_path):
     ref[iu, ju] = d
     ref[ju, iu] = d
     np.testing.assert_array_equal(m2, ref)  # bitwise: schedule-independent
+
+
+def test_merge_best_lexicographic_ties():
+    from paper_1707_02423_b200.distributed import merge_best
+    d = np.array([[1.5, 1.2, 2.0], [1.5, 1.3, 1.9], [1.4, 1.2, 2.0]])
+    i = np.array([[3, 1, 0], [10, 12, 11], [25, 27, 20]], np.int64)
+    bd, bi = merge_best(d, i)
+    np.testing.assert_array_equal(np.asarray(bd), [1.4, 1.2, 1.9])
+    np.testing.assert_array_equal(np.asarray(bi), [25, 1, 11])  # tie on 1.2 -> lowest corpus index
+
+
+def _nearest_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    import sys
+    sys.path.insert(0, str(REPO))
+    from oracle import ffi
+    from paper_1707_02423_b200 import synth
+    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.distributed import nearest_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q = synth.random_corpus(5, 4, 10, seed=7)
+    c = synth.random_corpus(23, 3, 12, seed=8) + [q[2].copy()]  # an exact match (d = min)
+    packed = pack(q + c)
+
+    def shard(c0, c1):
+        bd, bi = [], []
+        for i in range(len(q)):
+            ia = np.full(c1 - c0, i, np.int32)
+            ib = np.arange(len(q) + c0, len(q) + c1, dtype=np.int32)
+            d, *_ = ffi.iso_batch(packed, ia, ib, threads=1)
+            j = int(np.argmin(d))
+            bd.append(d[j])
+            bi.append(c0 + j)
+        return np.array(bd), np.array(bi, np.int64)
+
+    bd, bi = nearest_sharded(len(c), shard)
+    if rank == 0:
+        np.save(out_path, np.concatenate([bd, bi.astype(float)]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_nearest_matches_single_rank(tmp_path):
+    import torch.multiprocessing as mp
+    import sys
+    sys.path.insert(0, str(REPO))
+    from oracle import ffi
+    from paper_1707_02423_b200 import synth
+    from paper_1707_02423_b200.corpus import pack
+
+    out = tmp_path / "n.npy"
+    mp.start_processes(_nearest_worker, args=(2, _free_port(), str(out)), nprocs=2, start_method="spawn")
+    got = np.load(out)
+    q = synth.random_corpus(5, 4, 10, seed=7)
+    c = synth.random_corpus(23, 3, 12, seed=8) + [q[2].copy()]
+    packed = pack(q + c)
+    for i in range(len(q)):
+        ia = np.full(len(c), i, np.int32)
+        ib = np.arange(len(q), len(q) + len(c), dtype=np.int32)
+        d, *_ = ffi.iso_batch(packed, ia, ib, threads=1)
+        assert got[i] == d.min()
+        assert int(got[len(q) + i]) == int(np.argmin(d))
