@@ -36,6 +36,7 @@ namespace cfgsim {
 constexpr int BIG_THREADS = 256;
 constexpr int BIG_WARPS = BIG_THREADS / 32;
 constexpr int BIG_TM = 128, BIG_TN = 64, BIG_KC = 16;  // GEMM tile and k-chunk
+constexpr int BIG_UP = BIG_TM + 8, BIG_VP = BIG_TN + 8;  // staged row pitches (== 8 mod 16 doubles)
 constexpr int BIG_CB = 10;                            // column bits of a sort key (N <= 1024)
 constexpr int BIG_R = 1024 / BIG_THREADS;             // greedy rows per thread
 
@@ -109,8 +110,8 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
   s.scr = take(sizeof(double) * 2 * nlim);  // operator build scratch (colW, rowAW)
   const size_t sweep_end = o;
   o = base;
-  s.us = take(sizeof(T) * 2 * BIG_KC * BIG_TM);  // double-buffered
-  s.vs = take(sizeof(T) * 2 * BIG_KC * BIG_TN);
+  s.us = take(sizeof(T) * 2 * BIG_KC * BIG_UP);  // double-buffered
+  s.vs = take(sizeof(T) * 2 * BIG_KC * BIG_VP);
   const size_t gemm_end = o;
   o = base;
   s.taken = take(sizeof(uint32_t) * 32);
@@ -299,17 +300,17 @@ __device__ __forceinline__ void big_cp_async_wait_group() { asm volatile("cp.asy
 
 // compare-exchange of registers c and c ^ J inside each lane (elements
 // e = lane * KB + c), direction by bit k of e
-template <int KB, int J>
-__device__ __forceinline__ void big_stage_reg(unsigned long long (&v)[KB], int lane, int k) {
+template <typename K, int KB, int J>
+__device__ __forceinline__ void big_stage_reg(K (&v)[KB], int lane, int k) {
 #pragma unroll
   for (int c = 0; c < KB; c++) {
     if ((c & J) == 0) {
       const int pc = c | J;
       const bool up = (((lane * KB + c) & k) == 0);
-      const unsigned long long a = v[c], b = v[pc];
-      const bool sw = up ? (b > a) : (a > b);
-      v[c] = sw ? b : a;
-      v[pc] = sw ? a : b;
+      const K a = v[c], b = v[pc];
+      const K hi = a > b ? a : b, lo = a > b ? b : a;
+      v[c] = up ? hi : lo;
+      v[pc] = up ? lo : hi;
     }
   }
 }
@@ -318,8 +319,8 @@ __device__ __forceinline__ void big_stage_reg(unsigned long long (&v)[KB], int l
 // (each lane holds a contiguous run, so only log2(32) of every merge's stages
 // cross lanes).  Stage loops stay rolled: the fully unrolled 1024-key network
 // does not fit the instruction cache.
-template <int KB>
-__device__ __forceinline__ void big_sort_desc(unsigned long long (&v)[KB], int lane) {
+template <typename K, int KB>
+__device__ __forceinline__ void big_sort_desc(K (&v)[KB], int lane) {
   constexpr int n = 32 * KB;
 #pragma unroll 1
   for (int k = 2; k <= n; k <<= 1) {
@@ -330,18 +331,18 @@ __device__ __forceinline__ void big_sort_desc(unsigned long long (&v)[KB], int l
         const bool lower = (lane & lm) == 0;
 #pragma unroll
         for (int c = 0; c < KB; c++) {
-          const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[c], lm);
+          const K o = __shfl_xor_sync(0xffffffffu, v[c], lm);
           const bool up = (((lane * KB + c) & k) == 0);
-          const unsigned long long hi = o > v[c] ? o : v[c], lo = o > v[c] ? v[c] : o;
+          const K hi = o > v[c] ? o : v[c], lo = o > v[c] ? v[c] : o;
           v[c] = (lower == up) ? hi : lo;
         }
       } else {
         switch (j) {
-          case 1: big_stage_reg<KB, 1>(v, lane, k); break;
-          case 2: if constexpr (KB > 2) big_stage_reg<KB, 2>(v, lane, k); break;
-          case 4: if constexpr (KB > 4) big_stage_reg<KB, 4>(v, lane, k); break;
-          case 8: if constexpr (KB > 8) big_stage_reg<KB, 8>(v, lane, k); break;
-          case 16: if constexpr (KB > 16) big_stage_reg<KB, 16>(v, lane, k); break;
+          case 1: big_stage_reg<K, KB, 1>(v, lane, k); break;
+          case 2: if constexpr (KB > 2) big_stage_reg<K, KB, 2>(v, lane, k); break;
+          case 4: if constexpr (KB > 4) big_stage_reg<K, KB, 4>(v, lane, k); break;
+          case 8: if constexpr (KB > 8) big_stage_reg<K, KB, 8>(v, lane, k); break;
+          case 16: if constexpr (KB > 16) big_stage_reg<K, KB, 16>(v, lane, k); break;
           default: break;
         }
       }
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         const int ty = tid >> 4, tx = tid & 15;
         const int nch = (K + BIG_KC) / BIG_KC;  // chunks covering m = 0..K
         auto stage = [&](int i0, int j0, int ch, int bufi) {
-          T *us = Us + bufi * BIG_KC * BIG_TM, *vs = Vs + bufi * BIG_KC * BIG_TN;
+          T *us = Us + bufi * BIG_KC * BIG_UP, *vs = Vs + bufi * BIG_KC * BIG_VP;
           for (int e = tid; e < BIG_KC * (BIG_TM + BIG_TN); e += NT) {
             int mm, x, lim;
             const T *src;
@@ -557,65 +558,124 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
             if (e < BIG_KC * BIG_TM) {
               mm = e / BIG_TM; x = e % BIG_TM; lim = N - i0;
               src = Uh + (size_t)(ch * BIG_KC + mm) * N + i0 + x;
-              dst = us + e;
+              dst = us + mm * BIG_UP + x;
             } else {
               const int f = e - BIG_KC * BIG_TM;
               mm = f / BIG_TN; x = f % BIG_TN; lim = N - j0;
               src = Vh + (size_t)(ch * BIG_KC + mm) * N + j0 + x;
-              dst = vs + f;
+              dst = vs + mm * BIG_VP + x;
             }
             const bool ok = (ch * BIG_KC + mm <= K) && x < lim;
             big_cp_async_zfill<sizeof(T)>(dst, ok ? (const void *)src : (const void *)Uh, ok);
           }
           big_cp_async_commit();
         };
-        for (int i0 = 0; i0 < N; i0 += BIG_TM)
-          for (int j0 = 0; j0 < N; j0 += BIG_TN) {
-            T acc[8][4];
+        if constexpr (sizeof(T) == 8) {
+          // fp64 tensor cores: mma.m8n8k4 is the fma chain over k in order
+          // (bitwise equal to the scalar m-ascending accumulation; probed:
+          // tools/probes/dmma_probe.cu).  8 warps as 4 x 2, 4 x 4 tiles each.
+          const int wr = warp & 3, wc = warp >> 2;
+          const int lr = lane >> 2, lk = lane & 3;
+          for (int i0 = 0; i0 < N; i0 += BIG_TM)
+            for (int j0 = 0; j0 < N; j0 += BIG_TN) {
+              double acc[4][4][2];
 #pragma unroll
-            for (int a = 0; a < 8; a++)
+              for (int x = 0; x < 4; x++)
 #pragma unroll
-              for (int b = 0; b < 4; b++) acc[a][b] = (T)0;
-            __syncthreads();  // previous tile done with both buffers
-            stage(i0, j0, 0, 0);
-            for (int ch = 0; ch < nch; ch++) {
-              if (ch + 1 < nch) {
-                stage(i0, j0, ch + 1, (ch + 1) & 1);
-                big_cp_async_wait_group<1>();
-              } else {
-                big_cp_async_wait_group<0>();
+                for (int y = 0; y < 4; y++) acc[x][y][0] = acc[x][y][1] = 0.0;
+              __syncthreads();  // previous tile done with both buffers
+              stage(i0, j0, 0, 0);
+              for (int ch = 0; ch < nch; ch++) {
+                if (ch + 1 < nch) {
+                  stage(i0, j0, ch + 1, (ch + 1) & 1);
+                  big_cp_async_wait_group<1>();
+                } else {
+                  big_cp_async_wait_group<0>();
+                }
+                __syncthreads();
+                const double *us = (const double *)Us + (ch & 1) * BIG_KC * BIG_UP;
+                const double *vs = (const double *)Vs + (ch & 1) * BIG_KC * BIG_VP;
+#pragma unroll
+                for (int k0 = 0; k0 < BIG_KC; k0 += 4) {
+                  double af[4], bf[4];
+#pragma unroll
+                  for (int x = 0; x < 4; x++) af[x] = us[(k0 + lk) * BIG_UP + wr * 32 + x * 8 + lr];
+#pragma unroll
+                  for (int y = 0; y < 4; y++) bf[y] = vs[(k0 + lk) * BIG_VP + wc * 32 + y * 8 + lr];
+#pragma unroll
+                  for (int x = 0; x < 4; x++)
+#pragma unroll
+                    for (int y = 0; y < 4; y++)
+                      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                   : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                                   : "d"(af[x]), "d"(bf[y]));
+                }
+                __syncthreads();  // buffer (ch & 1) is re-staged by chunk ch + 2
               }
-              __syncthreads();
-              const T *us = Us + (ch & 1) * BIG_KC * BIG_TM, *vs = Vs + (ch & 1) * BIG_KC * BIG_TN;
 #pragma unroll
-              for (int mm = 0; mm < BIG_KC; mm++) {
-                T ua[8], vb[4];
+              for (int x = 0; x < 4; x++)
 #pragma unroll
-                for (int a = 0; a < 8; a++) ua[a] = us[mm * BIG_TM + ty + 16 * a];
+                for (int y = 0; y < 4; y++)
 #pragma unroll
-                for (int b = 0; b < 4; b++) vb[b] = vs[mm * BIG_TN + tx + 16 * b];
-#pragma unroll
-                for (int a = 0; a < 8; a++)
-#pragma unroll
-                  for (int b = 0; b < 4; b++) acc[a][b] = fma(ua[a], vb[b], acc[a][b]);
-              }
-              __syncthreads();  // buffer (ch & 1) is re-staged by chunk ch + 2
+                  for (int h = 0; h < 2; h++) {
+                    const int i = i0 + wr * 32 + x * 8 + lr, j = j0 + wc * 32 + y * 8 + 2 * lk + h;
+                    if (i < N && j < N) {
+                      X[(size_t)i * N + j] = (T)acc[x][y][h];
+                      const int e = big_exponent(acc[x][y][h]);
+                      emin = min(emin, e);
+                      emax = max(emax, e);
+                    }
+                  }
             }
+        } else {
+        for (int i0 = 0; i0 < N; i0 += BIG_TM)
+            for (int j0 = 0; j0 < N; j0 += BIG_TN) {
+              T acc[8][4];
 #pragma unroll
-            for (int a = 0; a < 8; a++) {
-              const int i = i0 + ty + 16 * a;
+              for (int a = 0; a < 8; a++)
 #pragma unroll
-              for (int b = 0; b < 4; b++) {
-                const int j = j0 + tx + 16 * b;
-                if (i < N && j < N) {
-                  X[(size_t)i * N + j] = acc[a][b];
-                  const int e = big_exponent(acc[a][b]);
-                  emin = min(emin, e);
-                  emax = max(emax, e);
+                for (int b = 0; b < 4; b++) acc[a][b] = (T)0;
+              __syncthreads();  // previous tile done with both buffers
+              stage(i0, j0, 0, 0);
+              for (int ch = 0; ch < nch; ch++) {
+                if (ch + 1 < nch) {
+                  stage(i0, j0, ch + 1, (ch + 1) & 1);
+                  big_cp_async_wait_group<1>();
+                } else {
+                  big_cp_async_wait_group<0>();
+                }
+                __syncthreads();
+                const T *us = Us + (ch & 1) * BIG_KC * BIG_UP, *vs = Vs + (ch & 1) * BIG_KC * BIG_VP;
+#pragma unroll
+                for (int mm = 0; mm < BIG_KC; mm++) {
+                  T ua[8], vb[4];
+#pragma unroll
+                  for (int a = 0; a < 8; a++) ua[a] = us[mm * BIG_UP + ty + 16 * a];
+#pragma unroll
+                  for (int b = 0; b < 4; b++) vb[b] = vs[mm * BIG_VP + tx + 16 * b];
+#pragma unroll
+                  for (int a = 0; a < 8; a++)
+#pragma unroll
+                    for (int b = 0; b < 4; b++) acc[a][b] = fma(ua[a], vb[b], acc[a][b]);
+                }
+                __syncthreads();  // buffer (ch & 1) is re-staged by chunk ch + 2
+              }
+#pragma unroll
+              for (int a = 0; a < 8; a++) {
+                const int i = i0 + ty + 16 * a;
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                  const int j = j0 + tx + 16 * b;
+                  if (i < N && j < N) {
+                    X[(size_t)i * N + j] = acc[a][b];
+                    const int e = big_exponent(acc[a][b]);
+                    emin = min(emin, e);
+                    emax = max(emax, e);
+                  }
                 }
               }
             }
-          }
+        }
       }
       {
         int *ered = (int *)(smem_raw + L.misc + 32);
@@ -640,55 +700,71 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       }
       __syncthreads();
 
-      // ---- 4a. row orders (value desc, column asc): warp bitonic sort of keys
+      // ---- 4a. row orders (value desc, column asc).  One warp per row sorts
+      // 32-bit keys (top 22 bits of the row-rebased value | inverted column),
+      // then gathers the exact values into pair-wide 64-bit keys in sorted
+      // order; equal 22-bit prefixes with different exact values (near-ties,
+      // ~1e-6 relative) are repaired by odd-even transposition on the exact
+      // keys.  Exactly tied values keep column order from the key's low bits.
       for (int i = warp; i < N; i += BIG_WARPS) {
         const T *row = X + (size_t)i * N;
-        unsigned long long key[KB];
+        int rmin = 0x7fffffff, rmax = -1;
+        for (int j = lane; j < N; j += 32) {
+          const int e = big_exponent(row[j]);
+          rmin = min(rmin, e);
+          rmax = max(rmax, e);
+        }
+        rmin = __reduce_min_sync(0xffffffffu, rmin);
+        rmax = __reduce_max_sync(0xffffffffu, rmax);
+        constexpr int MB = sizeof(T) == 8 ? 52 : 23;
+        const int rshift = (32 - __clz(rmax - rmin)) + MB - 22;  // value bits above the 22 kept
+        uint32_t key[KB];
 #pragma unroll
         for (int c = 0; c < KB; c++) {
           const int j = lane * KB + c;
-          key[c] = (j < N) ? big_sort_key<T>(row[j], j, emin, shift) : 0ull;  // padding sorts last
+          uint32_t k = 0u;  // padding sorts last (a real key's column field is >= 1024 - N >= 1 then)
+          if (j < N) {
+            const unsigned long long b = big_bits(row[j]);
+            const unsigned long long v =
+                ((((b >> MB) & (sizeof(T) == 8 ? 0x7ffull : 0xffull)) - (unsigned long long)rmin) << MB) |
+                (b & ((1ull << MB) - 1));
+            k = ((uint32_t)(v >> rshift) << BIG_CB) | (uint32_t)((1 << BIG_CB) - 1 - j);
+          }
+          key[c] = k;
         }
-        big_sort_desc<KB>(key, lane);
-        unsigned long long *o = skey + (size_t)i * N;
-        bool tie = false;
+        big_sort_desc<uint32_t, KB>(key, lane);
+        // exact pair-wide keys in sorted order
+        unsigned long long ek[KB];
 #pragma unroll
         for (int c = 0; c < KB; c++) {
           const int pos = lane * KB + c;
-          if (pos < N) o[pos] = key[c];
-          if (shift > 0 && c + 1 < KB && pos + 1 < N && (key[c] >> BIG_CB) == (key[c + 1] >> BIG_CB)) {
-            // equal truncated value: misordered only if the exact values differ
-            if (row[big_key_col(key[c])] != row[big_key_col(key[c + 1])]) tie = true;
-          }
+          const int col = (1 << BIG_CB) - 1 - (int)(key[c] & ((1u << BIG_CB) - 1));
+          ek[c] = (pos < N) ? big_sort_key<T>(row[col], col, emin, shift) : 0ull;
         }
-        if (shift > 0) {  // chunk boundary: last of this lane vs first of the next lane
-          const unsigned long long nk = __shfl_down_sync(0xffffffffu, key[0], 1);
-          const int pos = lane * KB + KB - 1;
-          if (lane < 31 && pos + 1 < N && (key[KB - 1] >> BIG_CB) == (nk >> BIG_CB) &&
-              row[big_key_col(key[KB - 1])] != row[big_key_col(nk)])
-            tie = true;
-        }
-        __syncwarp();
-        if (__any_sync(0xffffffffu, tie) && lane == 0) {
-          // insertion pass on exact (value desc, column asc); keys are already
-          // ordered up to the dropped bits, so only near-tied runs move
-          for (int p = 1; p < N; p++) {
-            const unsigned long long kp = o[p];
-            const int cp = big_key_col(kp);
-            const T vp = row[cp];
-            int q = p - 1;
-            while (q >= 0) {
-              const unsigned long long kq = o[q];
-              const int cq = big_key_col(kq);
-              const T vq = row[cq];
-              if (vq > vp || (vq == vp && cq < cp)) break;
-              o[q + 1] = kq;
-              q--;
+        // repair inversions among equal prefixes (exact keys descend strictly)
+        for (int pass = 0;; pass++) {
+          bool sw = false;
+#pragma unroll
+          for (int c = (pass & 1); c + 1 < KB; c += 2)
+            if (ek[c] < ek[c + 1]) {
+              const unsigned long long t = ek[c]; ek[c] = ek[c + 1]; ek[c + 1] = t;
+              sw = true;
             }
-            o[q + 1] = kp;
+          // lane boundary: last of lane l vs first of lane l + 1 (positions KB*l + KB-1, KB*(l+1))
+          if (((KB - 1) & 1) == (pass & 1)) {
+            const unsigned long long nxt = __shfl_down_sync(0xffffffffu, ek[0], 1);
+            const unsigned long long prv = __shfl_up_sync(0xffffffffu, ek[KB - 1], 1);
+            if (lane < 31 && ek[KB - 1] < nxt) { ek[KB - 1] = nxt; sw = true; }
+            if (lane > 0 && prv < ek[0]) { ek[0] = prv; sw = true; }
           }
+          if (!__any_sync(0xffffffffu, sw) && pass > 0) break;
         }
-        __syncwarp();
+        unsigned long long *o = skey + (size_t)i * N;
+#pragma unroll
+        for (int c = 0; c < KB; c++) {
+          const int pos = lane * KB + c;
+          if (pos < N) o[pos] = ek[c];
+        }
       }
       __syncthreads();
 
