@@ -449,79 +449,90 @@ bool use_twostage() {
   return on;
 }
 
-template <typename T>
-int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_params *p, double *d_lin,
-                   int32_t *iters_lin, int64_t out_base, int &launch_no, cudaStream_t st) {
-  Scratch &S = scratch_for(c->device);
-  const bool f32 = sizeof(T) == 4;
-  const double tol = f32 ? std::max(p->tol, p->tol_fp32) : p->tol;
-  const int kcap = big_kcap(p->alpha, tol, p->max_iter);
-  const auto &rs = c->row_start;
-  const int a0 = (int)(std::upper_bound(rs.begin(), rs.end(), us) - rs.begin()) - 1;
-  const int a1 = (int)(std::upper_bound(rs.begin(), rs.end(), ue - 1) - rs.begin()) - 1;
-  // groups of equal N among rows a0..a1; combos (perm[b], N) for b >= first row
-  struct Grp { int N, ra, rb; int64_t cbase; };
-  std::vector<Grp> grps;
-  std::vector<int32_t> cg, cn;
+// Combo table of one two-stage run (host side).
+struct SeqTable {
+  std::vector<int32_t> g, n;
   std::vector<int64_t> uoff;
   int64_t utot = 0;
-  for (int a = a0; a <= a1;) {
-    const int N = c->n_sorted[a];
-    int b = a;
-    while (b + 1 <= a1 && c->n_sorted[b + 1] == N) b++;
-    const int64_t base = (int64_t)cg.size();
-    grps.push_back({N, a, b, base - a});
-    for (int q = a; q < c->K; q++) {
-      cg.push_back(c->perm[q]);
-      cn.push_back(N);
-      uoff.push_back(utot);
-      utot += (int64_t)(kcap + 1) * seq_pitch<T>(N);
-    }
-    a = b + 1;
+  template <typename T>
+  void add(int32_t graph, int N, int kcap) {
+    g.push_back(graph);
+    n.push_back(N);
+    uoff.push_back(utot);
+    utot += (int64_t)(kcap + 1) * seq_pitch<T>(N);
   }
-  const int64_t nc = (int64_t)cg.size();
-  auto grow = [&](DBuf &b, size_t bytes) -> cudaError_t {
-    if (b.n >= bytes) return cudaSuccess;
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return e;
-    return b.alloc(bytes);
-  };
-  CU(grow(S.seq_u, sizeof(T) * (size_t)utot));
-  CU(grow(S.seq_d, sizeof(double) * (size_t)nc * (kcap + 1)));
-  CU(grow(S.seq_g, sizeof(int32_t) * nc));
-  CU(grow(S.seq_n, sizeof(int32_t) * nc));
-  CU(grow(S.seq_off, sizeof(int64_t) * nc));
-  CU(grow(S.seq_st, sizeof(int32_t) * nc));
-  CU(cudaMemcpyAsync(S.seq_g.p, cg.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(S.seq_n.p, cn.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(S.seq_off.p, uoff.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
-  {  // alpha^m by sequential products (the pair kernels' order)
-    std::vector<double> apow(kcap + 2);
-    apow[0] = 1.0;
-    for (int m = 1; m <= kcap + 1; m++) apow[m] = apow[m - 1] * p->alpha;
-    CU(grow(S.seq_apow, sizeof(double) * apow.size()));
-    CU(cudaMemcpyAsync(S.seq_apow.p, apow.data(), sizeof(double) * apow.size(), cudaMemcpyHostToDevice, st));
-  }
+};
 
+cudaError_t grow_buf(DBuf &b, size_t bytes, cudaStream_t st) {
+  if (b.n >= bytes) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(st);  // a previous launch may still read the old buffer
+  if (e != cudaSuccess) return e;
+  return b.alloc(bytes);
+}
+
+struct SeqRun {
+  double tol, eps;
+  int kcap;
+};
+
+template <typename T>
+SeqRun seq_run_params(const cfgsim_params *p) {
+  SeqRun r;
+  r.tol = sizeof(T) == 4 ? std::max(p->tol, p->tol_fp32) : p->tol;
+  r.eps = sizeof(T) == 4 ? 0.02 : 1e-6;
+  r.kcap = big_kcap(p->alpha, r.tol, p->max_iter);
+  return r;
+}
+
+// Upload a combo table and the alpha^m table.
+template <typename T>
+int seq_upload(Scratch &S, const SeqTable &tb, const SeqRun &rr, const cfgsim_params *p, cudaStream_t st) {
+  const int64_t nc = (int64_t)tb.g.size();
+  CU(grow_buf(S.seq_u, sizeof(T) * (size_t)std::max<int64_t>(tb.utot, 1), st));
+  CU(grow_buf(S.seq_d, sizeof(double) * (size_t)std::max<int64_t>(nc, 1) * (rr.kcap + 1), st));
+  CU(grow_buf(S.seq_g, sizeof(int32_t) * std::max<int64_t>(nc, 1), st));
+  CU(grow_buf(S.seq_n, sizeof(int32_t) * std::max<int64_t>(nc, 1), st));
+  CU(grow_buf(S.seq_off, sizeof(int64_t) * std::max<int64_t>(nc, 1), st));
+  CU(grow_buf(S.seq_st, sizeof(int32_t) * std::max<int64_t>(nc, 1), st));
+  CU(cudaMemcpyAsync(S.seq_g.p, tb.g.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(S.seq_n.p, tb.n.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(S.seq_off.p, tb.uoff.data(), sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
+  std::vector<double> apow(rr.kcap + 2);  // alpha^m by sequential products (the pair kernels' order)
+  apow[0] = 1.0;
+  for (int m = 1; m <= rr.kcap + 1; m++) apow[m] = apow[m - 1] * p->alpha;
+  CU(grow_buf(S.seq_apow, sizeof(double) * apow.size(), st));
+  CU(cudaMemcpyAsync(S.seq_apow.p, apow.data(), sizeof(double) * apow.size(), cudaMemcpyHostToDevice, st));
+  return CFGSIM_OK;
+}
+
+// Stage 1 for combos [id0, id0 + n), all graphs of corpus C; combos whose
+// operator lists overflow are re-run with dense-bound lists.
+template <typename T>
+int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr, const cfgsim_params *p, Scratch &S,
+               cudaStream_t st) {
+  if (n <= 0) return CFGSIM_OK;
   int dev, sms = 0;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // ---- stage 1
   SeqParams sp;
   sp.alpha = p->alpha;
-  sp.tol = tol;
-  sp.eps = f32 ? 0.02 : 1e-6;
+  sp.tol = rr.tol;
+  sp.eps = rr.eps;
   sp.max_iter = p->max_iter;
-  sp.kcap = kcap;
+  sp.kcap = rr.kcap;
   sp.nlim = kSeqNmax;
   SeqCombos cb;
-  cb.n = nc;
+  cb.n = n;
+  cb.id0 = id0;
   cb.list = nullptr;
   cb.g = S.seq_g.as<int32_t>();
   cb.nn = S.seq_n.as<int32_t>();
   cb.uoff = S.seq_off.as<int64_t>();
   cb.status = S.seq_st.as<int32_t>();
   const void *f1 = (const void *)isorank_seq_kernel<T, 2>;
+  DevCorpus dc = C->dev();
+  T *useq = S.seq_u.as<T>();
+  double *dseq = S.seq_d.as<double>();
   for (int pass = 0; pass < 2; pass++) {
     sp.cap = pass == 0 ? 14 * kSeqNmax + 16 : kSeqNmax * kSeqNmax;
     const size_t smem = seq_smem_layout<T>(kSeqNmax, sp.cap).total;
@@ -530,57 +541,100 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f1, 128, smem));
     if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-1 kernel cannot be resident");
     const int64_t grid = std::min<int64_t>((int64_t)sms * occ, cb.n);
-    T *useq = S.seq_u.as<T>();
-    double *dseq = S.seq_d.as<double>();
-    DevCorpus dc = c->dev();
     void *args[] = {(void *)&dc, (void *)&cb, (void *)&sp, (void *)&useq, (void *)&dseq};
     CU(cudaLaunchKernel(f1, dim3((unsigned)grid), dim3(128), args, smem, st));
     g_launches++;
     if (pass == 1) break;
-    std::vector<int32_t> stv(nc);
-    CU(cudaMemcpyAsync(stv.data(), S.seq_st.p, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> stv(n);
+    CU(cudaMemcpyAsync(stv.data(), S.seq_st.as<int32_t>() + id0, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     std::vector<int64_t> redo;
-    for (int64_t q = 0; q < nc; q++)
-      if (stv[q]) redo.push_back(q);
+    for (int64_t q = 0; q < n; q++)
+      if (stv[q]) redo.push_back(id0 + q);
     if (redo.empty()) break;
-    CU(grow(S.seq_list, sizeof(int64_t) * redo.size()));
+    CU(grow_buf(S.seq_list, sizeof(int64_t) * redo.size(), st));
     CU(cudaMemcpyAsync(S.seq_list.p, redo.data(), sizeof(int64_t) * redo.size(), cudaMemcpyHostToDevice, st));
     cb.n = (int64_t)redo.size();
     cb.list = S.seq_list.as<int64_t>();
   }
-  // ---- stage 2: one launch per N
+  return CFGSIM_OK;
+}
+
+// Stage 2 over `w` (triangle units or query x corpus rectangles) of one N.
+template <typename T>
+int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const PairOut &o, const SeqRun &rr,
+               const cfgsim_params *p, Scratch &S, int &launch_no, cudaStream_t st) {
+  if (w.n_items <= 0) return CFGSIM_OK;
+  int dev, sms = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const bool small = N <= 32;
+  const int ar = 4, bc = small ? 4 : 8, pw = small ? 2 : 4;  // producer warps (+1 consumer warp)
+  Pair2Params pp;
+  pp.alpha = p->alpha;
+  pp.tol = rr.tol;
+  pp.eps = rr.eps;
+  pp.max_iter = p->max_iter;
+  pp.kcap = rr.kcap;
+  pp.N = N;
+  pp.ty = (N + ar - 1) / ar;
+  pp.tx = (N + bc - 1) / bc;
+  pp.cbase = cbase;
+  pp.cbase2 = cbase2;
+  pp.apow = S.seq_apow.as<double>();
+  const int nt = 32 * (pw + 1);
+  static const int minb_env = [] {  // CFGSIM_P2_OCC=2|3: CTAs/SM the stage-2 kernel is compiled for
+    const char *e = getenv("CFGSIM_P2_OCC");
+    return e ? atoi(e) : 3;
+  }();
+  const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
+                                          : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
+                         : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
+                                          : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
+  const size_t smem = p2_smem_bytes(N, sizeof(T));
+  CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f2, nt, smem));
+  if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-2 kernel cannot be resident");
+  const int64_t grid = std::min<int64_t>((int64_t)sms * occ, w.n_items);
+  unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no++ % 64);
+  CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+  const int32_t *nn = nullptr;
+  const T *useq = S.seq_u.as<T>();
+  const double *dseq = S.seq_d.as<double>();
+  const int64_t *uo = S.seq_off.as<int64_t>();
+  void *args[] = {(void *)&nn, (void *)&w, (void *)&o, (void *)&pp, (void *)&useq, (void *)&dseq, (void *)&uo,
+                  (void *)&ctr};
+  CU(cudaLaunchKernel(f2, dim3((unsigned)grid), dim3(nt), args, smem, st));
+  g_launches++;
+  return CFGSIM_OK;
+}
+
+template <typename T>
+int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_params *p, double *d_lin,
+                   int32_t *iters_lin, int64_t out_base, int &launch_no, cudaStream_t st) {
+  Scratch &S = scratch_for(c->device);
+  const SeqRun rr = seq_run_params<T>(p);
+  const auto &rs = c->row_start;
+  const int a0 = (int)(std::upper_bound(rs.begin(), rs.end(), us) - rs.begin()) - 1;
+  const int a1 = (int)(std::upper_bound(rs.begin(), rs.end(), ue - 1) - rs.begin()) - 1;
+  // groups of equal N among rows a0..a1; combos (perm[b], N) for b >= the group's first row
+  struct Grp { int N, ra, rb; int64_t cbase; };
+  std::vector<Grp> grps;
+  SeqTable tb;
+  for (int a = a0; a <= a1;) {
+    const int N = c->n_sorted[a];
+    int b = a;
+    while (b + 1 <= a1 && c->n_sorted[b + 1] == N) b++;
+    grps.push_back({N, a, b, (int64_t)tb.g.size() - a});
+    for (int q = a; q < c->K; q++) tb.add<T>(c->perm[q], N, rr.kcap);
+    a = b + 1;
+  }
+  if (int rc = seq_upload<T>(S, tb, rr, p, st)) return rc;
+  if (int rc = seq_stage1<T>(c, 0, (int64_t)tb.g.size(), rr, p, S, st)) return rc;
   for (const Grp &gp : grps) {
     const int64_t gu0 = std::max(us, rs[gp.ra]), gu1 = std::min(ue, rs[gp.rb + 1]);
     if (gu1 <= gu0) continue;
-    const int N = gp.N;
-    const bool small = N <= 32;
-    const int ar = 4, bc = small ? 4 : 8, pw = small ? 2 : 4;  // producer warps (+1 consumer warp)
-    Pair2Params pp;
-    pp.alpha = p->alpha;
-    pp.tol = tol;
-    pp.eps = f32 ? 0.02 : 1e-6;
-    pp.max_iter = p->max_iter;
-    pp.kcap = kcap;
-    pp.N = N;
-    pp.ty = (N + ar - 1) / ar;
-    pp.tx = (N + bc - 1) / bc;
-    pp.cbase = gp.cbase;
-    const int nt = 32 * (pw + 1);
-    static const int minb_env = [] {  // CFGSIM_P2_OCC=2|3: CTAs/SM the stage-2 kernel is compiled for
-      const char *e = getenv("CFGSIM_P2_OCC");
-      return e ? atoi(e) : 3;
-    }();
-    const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
-                                            : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
-                           : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
-                                            : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
-    const size_t smem = p2_smem_bytes(N, sizeof(T));
-    pp.apow = S.seq_apow.as<double>();
-    CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f2, nt, smem));
-    if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-2 kernel cannot be resident");
     PairWork w{};
     w.mode = WORK_TRIANGLE;
     w.ordered = 0;
@@ -593,17 +647,63 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
     PairOut o{};
     o.d = d_lin;
     o.iters = iters_lin;
-    const int64_t grid = std::min<int64_t>((int64_t)sms * occ, w.n_items);
-    unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no++ % 64);
-    CU(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-    const int32_t *nn = c->d_n.as<int32_t>();
-    const T *useq = S.seq_u.as<T>();
-    const double *dseq = S.seq_d.as<double>();
-    const int64_t *uo = S.seq_off.as<int64_t>();
-    void *args[] = {(void *)&nn, (void *)&w, (void *)&o, (void *)&pp, (void *)&useq, (void *)&dseq, (void *)&uo,
-                    (void *)&ctr};
-    CU(cudaLaunchKernel(f2, dim3((unsigned)grid), dim3(nt), args, smem, st));
-    g_launches++;
+    if (int rc = seq_stage2<T>(gp.N, gp.cbase, 0, w, o, rr, p, S, launch_no, st)) return rc;
+  }
+  return CFGSIM_OK;
+}
+
+// Query-vs-corpus block through the two-stage path: for each N <= 64 the
+// combos of queries and corpus graphs with n <= N, then the rectangles
+// {n_q == N} x {n_c <= N} and {n_q < N} x {n_c == N} (sorted positions).
+template <typename T>
+int seq_nearest_t(const cfgsim_corpus *Q, const cfgsim_corpus *C, const std::vector<int32_t> &qs,
+                  const std::vector<int32_t> &cs, const int32_t *dqs, const int32_t *dcs, int32_t q0, int32_t c0,
+                  int32_t nc, const std::vector<int> &ns, const cfgsim_params *p, double *dm, int &launch_no,
+                  cudaStream_t st) {
+  Scratch &S = scratch_for(Q->device);
+  const SeqRun rr = seq_run_params<T>(p);
+  auto cnt = [](const std::vector<int32_t> &v, const cfgsim_corpus *X, int n, bool le) {
+    return (int32_t)((le ? std::upper_bound(v.begin(), v.end(), n, [&](int t, int x) { return t < X->n_nodes[x]; })
+                         : std::lower_bound(v.begin(), v.end(), n, [&](int x, int t) { return X->n_nodes[x] < t; })) -
+                     v.begin());
+  };
+  for (int N : ns) {
+    const int32_t qlt = cnt(qs, Q, N, false), qle = cnt(qs, Q, N, true);
+    const int32_t clt = cnt(cs, C, N, false), cle = cnt(cs, C, N, true);
+    std::vector<int32_t> rects;
+    if (qle > qlt && cle > 0) rects.insert(rects.end(), {qlt, qle, 0, cle});
+    if (qlt > 0 && cle > clt) rects.insert(rects.end(), {0, qlt, clt, cle});
+    if (rects.empty()) continue;
+    SeqTable tb;  // [queries with n <= N | corpus graphs with n <= N], sorted positions
+    for (int32_t q = 0; q < qle; q++) tb.add<T>(qs[q], N, rr.kcap);
+    for (int32_t x = 0; x < cle; x++) tb.add<T>(cs[x], N, rr.kcap);
+    if (int rc = seq_upload<T>(S, tb, rr, p, st)) return rc;
+    if (int rc = seq_stage1<T>(Q, 0, qle, rr, p, S, st)) return rc;
+    if (int rc = seq_stage1<T>(C, qle, cle, rr, p, S, st)) return rc;
+    const int nr = (int)rects.size() / 4;
+    std::vector<int64_t> rsum(nr + 1, 0);
+    for (int r = 0; r < nr; r++)
+      rsum[r + 1] = rsum[r] + (int64_t)(rects[4 * r + 1] - rects[4 * r]) * (rects[4 * r + 3] - rects[4 * r + 2]);
+    DBuf drs, drect;
+    CU(drs.alloc(sizeof(int64_t) * (nr + 1)));
+    CU(drect.alloc(sizeof(int32_t) * 4 * nr));
+    CU(cudaMemcpyAsync(drs.p, rsum.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(drect.p, rects.data(), sizeof(int32_t) * 4 * nr, cudaMemcpyHostToDevice, st));
+    PairWork w{};
+    w.mode = WORK_RECT;
+    w.n_items = rsum[nr];
+    w.nrect = nr;
+    w.rect_start = drs.as<int64_t>();
+    w.rect = drect.as<int32_t>();
+    w.qperm = dqs;
+    w.cperm = dcs;
+    w.qbase = q0;
+    w.cbase = c0;
+    w.ld = nc;
+    PairOut o{};
+    o.d = dm;
+    if (int rc = seq_stage2<T>(N, 0, qle, w, o, rr, p, S, launch_no, st)) return rc;
+    CU(cudaStreamSynchronize(st));  // drs / drect and the combo buffers are reused by the next N
   }
   return CFGSIM_OK;
 }
@@ -1364,7 +1464,23 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
                            : std::lower_bound(cs.begin(), cs.end(), n, [&](int x, int v) { return C->n_nodes[x] < v; })) -
                        cs.begin());
     };
+    // N <= 64: two-stage path (per-(graph, N) sequences, then per-pair rank-K products)
+    const double tol_eff = p->precision == CFGSIM_FP32 ? std::max(p->tol, p->tol_fp32) : p->tol;
+    const bool two = lr && use_twostage() && big_kcap(p->alpha, tol_eff, p->max_iter) <= 512;
+    int launch_no2 = 0;
+    if (two) {
+      std::vector<int> small;
+      for (int N : ns)
+        if (N <= kSeqNmax) small.push_back(N);
+      const int rc = p->precision == CFGSIM_FP32
+                         ? seq_nearest_t<float>(Q, C, qs, cs, dqs.as<int32_t>(), dcs.as<int32_t>(), q0, c0, nc, small,
+                                                p, dm.as<double>(), launch_no2, st)
+                         : seq_nearest_t<double>(Q, C, qs, cs, dqs.as<int32_t>(), dcs.as<int32_t>(), q0, c0, nc, small,
+                                                 p, dm.as<double>(), launch_no2, st);
+      if (rc) return rc;
+    }
     for (int N : ns) {
+      if (two && N <= kSeqNmax) continue;
       if (N > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
       const int key = (!lr || lr_supported(p->precision, N)) ? N : kBigKey + big_kb(N);
       if (launches.empty() || launches.back().key != key) launches.push_back({key, N, {}});

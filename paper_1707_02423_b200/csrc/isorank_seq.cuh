@@ -42,7 +42,8 @@ struct SeqParams {
 // at dseq[c * (kcap + 1) + m].
 struct SeqCombos {
   int64_t n;
-  const int64_t *list;  // NULL: combos 0..n-1, else the combo ids to build
+  int64_t id0;          // combos id0 .. id0 + n - 1 (when list == NULL)
+  const int64_t *list;  // else the combo ids to build
   const int32_t *g;
   const int32_t *nn;
   const int64_t *uoff;
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(64 * KB) isorank_seq_kernel(DevCorpus C, SeqCo
   const int NW = blockDim.x >> 5;
 
   for (int64_t ci = blockIdx.x; ci < cb.n; ci += gridDim.x) {
-    const int64_t c = cb.list ? cb.list[ci] : ci;
+    const int64_t c = cb.list ? cb.list[ci] : cb.id0 + ci;
     const int g = cb.g[c], N = cb.nn[c];
     int32_t *nz = misc + 1;
     const bool ok = build_side<T, KB, 1, false>(C, g, N, N | 1, dense, lo_s, fr_s, zflag, zl, nz, toff, nullptr,
@@ -161,7 +162,8 @@ struct Pair2Params {
   int32_t kcap;
   int32_t N;
   int32_t ty, tx;   // thread grid of the AR x BC entry blocks
-  int64_t cbase;    // combo index = cbase + sorted position
+  int64_t cbase;    // combo index = cbase + sorted position (triangle; rect: query side)
+  int64_t cbase2;   // rect mode: combo index of the corpus side = cbase2 + sorted position
   const double *apow;  // alpha^m, m = 0..kcap, by sequential products (host)
 };
 
@@ -590,19 +592,37 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     T *Xs = (T *)(smem_raw + L.x[s]);
     T *stg = Xs;
     uint8_t *ord = smem_raw + L.ord[s];
-    // triangle unit -> sorted rows a <= b; the alignment runs in the caller's
-    // (lower graph index, higher graph index) direction
-    const int64_t uu = work.u0 + item;
-    int lo = 0, hi = work.K - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (work.row_start[mid] <= uu) lo = mid; else hi = mid - 1;
+    int64_t slot, ca, cb;
+    if (work.mode == WORK_RECT) {
+      // (query, corpus) rectangle in size-sorted positions; A = the query
+      int lo = 0, hi = work.nrect - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (work.rect_start[mid] <= item) lo = mid; else hi = mid - 1;
+      }
+      const int32_t *R = work.rect + 4 * lo;
+      const int64_t loc = item - work.rect_start[lo];
+      const int w = R[3] - R[2];
+      const int q = R[0] + (int)(loc / w), cc = R[2] + (int)(loc % w);
+      slot = (int64_t)(work.qperm[q] - work.qbase) * work.ld + (work.cperm[cc] - work.cbase);
+      ca = prm.cbase + q;
+      cb = prm.cbase2 + cc;
+    } else {
+      // triangle unit -> sorted rows a <= b; the alignment runs in the caller's
+      // (lower graph index, higher graph index) direction
+      const int64_t uu = work.u0 + item;
+      int lo = 0, hi = work.K - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (work.row_start[mid] <= uu) lo = mid; else hi = mid - 1;
+      }
+      const int a = lo, b = a + (int)(uu - work.row_start[a]);
+      int pa = a, pb = b;
+      if (work.perm[pa] > work.perm[pb]) { const int t = pa; pa = pb; pb = t; }
+      slot = uu - work.out_base;
+      ca = prm.cbase + pa;
+      cb = prm.cbase + pb;
     }
-    const int a = lo, b = a + (int)(uu - work.row_start[a]);
-    int pa = a, pb = b;
-    if (work.perm[pa] > work.perm[pb]) { const int t = pa; pa = pb; pb = t; }
-    const int64_t slot = uu - work.out_base;
-    const int64_t ca = prm.cbase + pa, cb = prm.cbase + pb;
     const T *UA = useq + uoff[ca];
     const T *UB = useq + uoff[cb];
     const double *DA = dseq + ca * (int64_t)(prm.kcap + 1);

@@ -325,3 +325,30 @@ def test_two_stage_matches_per_pair_kernel(P):
         n = len(outs[0]) // 2
         np.testing.assert_array_equal(outs[0][n:], outs[1][n:])
         np.testing.assert_array_equal(outs[0][:n], outs[1][:n])
+
+
+def test_nearest_mixed_sizes_matches_oracle(P):
+    """Query-vs-corpus over sizes spanning the two-stage (N <= 64), per-pair
+    low-rank (65..128) and large-N (> 128) kernels, fp64 and fp32."""
+    from oracle import ffi
+    from paper_1707_02423_b200 import synth
+    rng = np.random.default_rng(41)
+    q = [synth.transition_matrix(synth.random_shape(rng, int(n), "sampled")) for n in (8, 30, 64, 90, 150)]
+    c = [synth.transition_matrix(synth.random_shape(rng, int(n), "sampled"))
+         for n in rng.integers(4, 180, 40)] + [q[1].copy(), q[3].copy()]
+    allm = q + c
+    packed = P.pack(allm)
+    ia = np.repeat(np.arange(len(q)), len(c)).astype(np.int32)
+    ib = np.tile(np.arange(len(q), len(allm)), len(q)).astype(np.int32)
+    d, *_ = ffi.iso_batch(packed, ia, ib)
+    d = d.reshape(len(q), len(c))
+    for prec, rtol in (("fp64", RTOL64), ("fp32", RTOL32)):
+        bd, bi = P.nearest(q, c, precision=prec)
+        np.testing.assert_allclose(bd, d.min(axis=1), rtol=rtol)
+        if prec == "fp64":
+            np.testing.assert_array_equal(bi, d.argmin(axis=1))
+    # the rectangle path and the per-pair list path agree bitwise
+    with P.DeviceCorpus(q) as CQ, P.DeviceCorpus(c) as CC:
+        dl, *_ = P.isorank_pairs(CQ, CC, np.repeat(np.arange(len(q)), len(c)), np.tile(np.arange(len(c)), len(q)))
+    bd, bi = P.nearest(q, c)
+    np.testing.assert_array_equal(bd, dl.reshape(len(q), len(c)).min(axis=1))
