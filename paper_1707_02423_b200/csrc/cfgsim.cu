@@ -415,10 +415,31 @@ int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, 
   prm.slab = S.gslab.as<unsigned char>();
   prm.slab_bytes = (int64_t)slab;
   prm.status = S.status.as<int32_t>();
+  static const bool phases = [] {
+    const char *e = getenv("CFGSIM_PHASES");
+    return e && atoi(e) != 0;
+  }();
+  static DBuf phase_buf;
+  prm.phase = nullptr;
+  if (phases) {
+    if (!phase_buf.p) CU(phase_buf.alloc(8 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(phase_buf.p, 0, 8 * sizeof(unsigned long long), st));
+    prm.phase = phase_buf.as<unsigned long long>();
+  }
   CU(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   void *args[] = {(void *)&A, (void *)&B, (void *)&work, (void *)&out, (void *)&prm, (void *)&counter};
   CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(BIG_THREADS), args, smem, st));
   g_launches++;
+  if (prm.phase) {
+    unsigned long long ph[8];
+    CU(cudaMemcpyAsync(ph, prm.phase, sizeof(ph), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    double tot = 0;
+    for (int k = 0; k < 5; k++) tot += (double)ph[k];
+    fprintf(stderr, "[cfgsim big N<=%d] phase cycles (sum over CTAs): operators %.1f%% sweeps %.1f%% gemm %.1f%% "
+            "sort %.1f%% greedy %.1f%% total %.3e | rounds %llu advances %llu deep %llu\n", nlim, 100 * ph[0] / tot,
+            100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot, tot, ph[7], ph[5], ph[6]);
+  }
   return CFGSIM_OK;
 }
 

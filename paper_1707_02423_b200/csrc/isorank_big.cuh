@@ -50,11 +50,12 @@ struct BigParams {
   unsigned char *slab;
   int64_t slab_bytes;  // per CTA
   int32_t *status;     // != 0: internal error (history overflow)
+  unsigned long long *phase;  // optional (CFGSIM_PHASES=1): cycles per phase, summed over CTAs
 };
 
 // per-CTA global slab
 struct BigSlab {
-  size_t coef, uh, vh, x, skey, total;
+  size_t coef, uh, vh, x, sval, scol, total;
 };
 
 template <typename T>
@@ -70,7 +71,8 @@ __host__ __device__ inline BigSlab big_slab_layout(int nlim, int kcap) {
   s.uh = take(sizeof(T) * (size_t)(kcap + 1) * nlim);
   s.vh = take(sizeof(T) * (size_t)(kcap + 1) * nlim);
   s.x = take(sizeof(T) * (size_t)nlim * nlim);
-  s.skey = take(sizeof(unsigned long long) * (size_t)nlim * nlim);
+  s.sval = take(sizeof(unsigned long long) * (size_t)nlim * nlim);  // sorted exact value bits
+  s.scol = take(sizeof(uint16_t) * (size_t)nlim * nlim);            // sorted columns
   s.total = o;
   return s;
 }
@@ -82,7 +84,7 @@ struct BigSmem {
   // gemm region
   size_t us, vs;
   // greedy region
-  size_t taken, gslot, mrow;
+  size_t taken, gslot, mrow, mval;
   size_t red, misc, total;
 };
 
@@ -117,6 +119,7 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
   s.taken = take(sizeof(uint32_t) * 32);
   s.gslot = take(sizeof(unsigned long long) * 2 * BIG_WARPS + sizeof(int32_t) * (4 * BIG_WARPS + 2));
   s.mrow = take(sizeof(int32_t) * nlim);
+  s.mval = take(sizeof(unsigned long long) * nlim);
   const size_t greedy_end = o;
   size_t e = sweep_end > gemm_end ? sweep_end : gemm_end;
   e = e > greedy_end ? e : greedy_end;
@@ -350,6 +353,16 @@ __device__ __forceinline__ void big_sort_desc(K (&v)[KB], int lane) {
   }
 }
 
+// per-phase cycle accounting (debug): phase k's time = clock at mark k+1 - mark k
+#define BIG_PHASE(k)                                                                  \
+  do {                                                                                \
+    if (prm.phase && threadIdx.x == 0) {                                              \
+      const unsigned long long now = clock64();                                       \
+      if ((k) > 0) atomicAdd(prm.phase + (k) - 1, now - t_phase);                      \
+      t_phase = now;                                                                  \
+    }                                                                                 \
+  } while (0)
+
 template <typename T, int KB>
 __global__ void __launch_bounds__(BIG_THREADS, 2)
     isorank_big_kernel(DevCorpus CA, DevCorpus CB, PairWork work, PairOut out, BigParams prm,
@@ -362,12 +375,14 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
   T *Uh = (T *)(slab + G.uh);
   T *Vh = (T *)(slab + G.vh);
   T *X = (T *)(slab + G.x);
-  unsigned long long *skey = (unsigned long long *)(slab + G.skey);
+  unsigned long long *sval = (unsigned long long *)(slab + G.sval);
+  uint16_t *scol = (uint16_t *)(slab + G.scol);
   double *red = (double *)(smem_raw + L.red);
   int64_t *s_item = (int64_t *)(smem_raw + L.misc);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = BIG_THREADS;
+  unsigned long long t_phase = 0;
 
   for (;;) {
     if (tid == 0) *s_item = (int64_t)atomicAdd(counter, 1ull);
@@ -386,6 +401,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       const int na = C1.n_nodes[g1], nb = C2.n_nodes[g2];
       const int N = na > nb ? na : nb;
 
+      BIG_PHASE(0);
       // ---- 1. operators
       BigSide SA, SB;
       auto setup = [&](BigSide &S, const DevCorpus &Cs, int g, int sd) {
@@ -410,6 +426,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       T *ring[2] = {(T *)(smem_raw + L.ring[0]), (T *)(smem_raw + L.ring[1])};
       T *tv[2] = {(T *)(smem_raw + L.t[0]), (T *)(smem_raw + L.t[1])};
 
+      BIG_PHASE(1);
       // ---- 2. sweeps
       for (int q = tid; q < N; q += NT) {
         ring[0][q] = (T)1;
@@ -536,6 +553,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       }
       __syncthreads();
 
+      BIG_PHASE(2);
       // ---- 3. X = sum_m coef_m u_m v_m^T  (128 x 64 tiles, 8 x 4 per thread,
       //         k-chunks of the histories double-buffered with cp.async);
       //         exponent range of X for the pair-wide sort keys.
@@ -700,6 +718,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       }
       __syncthreads();
 
+      BIG_PHASE(3);
       // ---- 4a. row orders (value desc, column asc).  One warp per row sorts
       // 32-bit keys (top 22 bits of the row-rebased value | inverted column),
       // then gathers the exact values into pair-wide 64-bit keys in sorted
@@ -733,7 +752,10 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           key[c] = k;
         }
         big_sort_desc<uint32_t, KB>(key, lane);
-        // exact pair-wide keys in sorted order
+        // pair-wide 64-bit keys (exponent | mantissa truncated by `shift` bits |
+        // column) in sorted order; odd-even transposition repairs inversions
+        // among equal 22-bit prefixes, then neighbours whose truncated keys
+        // tie are put in exact (value desc, column asc) order from X
         unsigned long long ek[KB];
 #pragma unroll
         for (int c = 0; c < KB; c++) {
@@ -741,176 +763,169 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           const int col = (1 << BIG_CB) - 1 - (int)(key[c] & ((1u << BIG_CB) - 1));
           ek[c] = (pos < N) ? big_sort_key<T>(row[col], col, emin, shift) : 0ull;
         }
-        // repair inversions among equal prefixes (exact keys descend strictly)
+        // `after(x, y)`: y must precede x — (value desc, column asc), exact:
+        // equal truncated values are decided on X (keys' low bits only hold
+        // the column, which ties exact values)
+        auto after = [&](unsigned long long x, unsigned long long y) {
+          if ((x >> BIG_CB) != (y >> BIG_CB)) return (x >> BIG_CB) < (y >> BIG_CB);
+          if (shift > 0) {
+            const T vx = row[big_key_col(x)], vy = row[big_key_col(y)];
+            if (vx != vy) return vx < vy;
+          }
+          return (x & ((1ull << BIG_CB) - 1)) < (y & ((1ull << BIG_CB) - 1));  // lower column first
+        };
         for (int pass = 0;; pass++) {
           bool sw = false;
 #pragma unroll
           for (int c = (pass & 1); c + 1 < KB; c += 2)
-            if (ek[c] < ek[c + 1]) {
+            if (lane * KB + c + 1 < N && after(ek[c], ek[c + 1])) {
               const unsigned long long t = ek[c]; ek[c] = ek[c + 1]; ek[c + 1] = t;
               sw = true;
             }
-          // lane boundary: last of lane l vs first of lane l + 1 (positions KB*l + KB-1, KB*(l+1))
-          if (((KB - 1) & 1) == (pass & 1)) {
-            const unsigned long long nxt = __shfl_down_sync(0xffffffffu, ek[0], 1);
-            const unsigned long long prv = __shfl_up_sync(0xffffffffu, ek[KB - 1], 1);
-            if (lane < 31 && ek[KB - 1] < nxt) { ek[KB - 1] = nxt; sw = true; }
-            if (lane > 0 && prv < ek[0]) { ek[0] = prv; sw = true; }
+          if (((KB - 1) & 1) == (pass & 1)) {  // lane boundary pair (KB*l + KB-1, KB*(l+1))
+            const unsigned long long nv = __shfl_down_sync(0xffffffffu, ek[0], 1);
+            const unsigned long long pv = __shfl_up_sync(0xffffffffu, ek[KB - 1], 1);
+            const bool xl = lane < 31 && lane * KB + KB < N && after(ek[KB - 1], nv);
+            const bool xr = lane > 0 && lane * KB < N && after(pv, ek[0]);
+            if (xl) { ek[KB - 1] = nv; sw = true; }
+            if (xr) { ek[0] = pv; sw = true; }
           }
-          if (!__any_sync(0xffffffffu, sw) && pass > 0) break;
+          if ((!__any_sync(0xffffffffu, sw) && pass > 0) || pass > 64 * KB) break;  // (bounded: odd-even transposition sorts in n passes)
         }
-        unsigned long long *o = skey + (size_t)i * N;
+        unsigned long long *ov = sval + (size_t)i * N;
+        uint16_t *oc = scol + (size_t)i * N;
 #pragma unroll
         for (int c = 0; c < KB; c++) {
           const int pos = lane * KB + c;
-          if (pos < N) o[pos] = ek[c];
+          if (pos < N) {
+            const int col = big_key_col(ek[c]);
+            ov[pos] = big_bits(row[col]);  // exact value bits for the rounds
+            oc[pos] = (uint16_t)col;
+          }
         }
       }
       __syncthreads();
 
+      BIG_PHASE(4);
       // ---- 4b. greedy matching rounds, similarity.py:96-108, whole CTA.
-      // Thread t owns rows t + 256 r (r < BIG_R).  Each active row's head is
-      // its best untaken column, held as a sort key (comparable across rows
-      // up to the dropped bits; equal truncated heads are resolved on exact
-      // values).  A round: per-warp best head -> shared slots -> every
-      // thread picks the same winner (value desc, row asc = np.argmax's
-      // first occurrence); rows whose head column was taken advance along
-      // their sorted keys (next key already loaded into a register).
+      // Thread t owns rows t + 256 r (r < BIG_R); each active row's head is
+      // its best untaken column, compared across rows on exact value bits
+      // with ties to the lowest row (np.argmax's first occurrence).  A round:
+      // per-warp best -> shared slots (value, row, column) -> one barrier ->
+      // every thread picks the same winner, marks the column, and advances
+      // its rows whose head column was taken.  The next three sorted entries
+      // of every row are already in registers (loads issued rounds earlier),
+      // so no HBM round trip sits on the per-round critical path.
       {
         uint32_t *taken = (uint32_t *)(smem_raw + L.taken);
-        unsigned long long *slot_k = (unsigned long long *)(smem_raw + L.gslot);
-        int32_t *slot_r = (int32_t *)(slot_k + 2 * BIG_WARPS);
-        int32_t *slot_n = slot_r + 2 * BIG_WARPS;
+        unsigned long long *slot_v = (unsigned long long *)(smem_raw + L.gslot);
+        int32_t *slot_r = (int32_t *)(slot_v + 2 * BIG_WARPS);
+        int32_t *slot_c = slot_r + 2 * BIG_WARPS;
         int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
+        unsigned long long *mval = (unsigned long long *)(smem_raw + L.mval);
         for (int w = tid; w < 32; w += NT) taken[w] = 0u;
-        unsigned long long hk[BIG_R], nk[BIG_R];
-        int ptr[BIG_R];
+        constexpr int PF = 3;  // prefetch depth (positions ahead of the head)
+        unsigned long long hv[BIG_R], qv[BIG_R][PF];
+        int hc[BIG_R], qc[BIG_R][PF], ptr[BIG_R];
         uint32_t act = 0u;
 #pragma unroll
         for (int r = 0; r < BIG_R; r++) {
           const int i = tid + BIG_THREADS * r;
-          hk[r] = nk[r] = 0ull;
+          hv[r] = 0ull;
+          hc[r] = 0;
           ptr[r] = 0;
+#pragma unroll
+          for (int f = 0; f < PF; f++) { qv[r][f] = 0ull; qc[r][f] = 0; }
           if (i < N) {
             act |= 1u << r;
-            hk[r] = skey[(size_t)i * N];
-            if (N > 1) nk[r] = skey[(size_t)i * N + 1];
+            hv[r] = sval[(size_t)i * N];
+            hc[r] = scol[(size_t)i * N];
+#pragma unroll
+            for (int f = 0; f < PF; f++)
+              if (1 + f < N) {
+                qv[r][f] = sval[(size_t)i * N + 1 + f];
+                qc[r][f] = scol[(size_t)i * N + 1 + f];
+              }
           }
         }
         __syncthreads();
+        if (prm.phase && tid == 0) atomicAdd(prm.phase + 7, (unsigned long long)N);
         for (int round = 0; round < N; round++) {
-          // local best (truncated value desc, row asc)
           unsigned long long bv = 0ull;
-          int brow = 0x7fffffff;
+          int brow = 0x7fffffff, bcl = 0;
 #pragma unroll
-          for (int r = 0; r < BIG_R; r++) {
-            const unsigned long long v = hk[r] >> BIG_CB;
-            if ((act >> r) & 1u) {
-              if (brow == 0x7fffffff || v > bv) { bv = v; brow = tid + BIG_THREADS * r; }
+          for (int r = 0; r < BIG_R; r++)
+            if (((act >> r) & 1u) && (brow == 0x7fffffff || hv[r] > bv)) {
+              bv = hv[r];
+              brow = tid + BIG_THREADS * r;
+              bcl = hc[r];
             }
-          }
           const bool has = brow != 0x7fffffff;
           const unsigned hi = (unsigned)(bv >> 32), lo = (unsigned)bv;
           const unsigned mhi = __reduce_max_sync(0xffffffffu, has ? hi : 0u);
           const unsigned mlo = __reduce_max_sync(0xffffffffu, (has && hi == mhi) ? lo : 0u);
           const bool cand = has && hi == mhi && lo == mlo;
           const int wrow = (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)brow : 0x7fffffffu);
-          // rows of this warp whose head has the warp's best truncated value
-          int cnt = 0;
-#pragma unroll
-          for (int r = 0; r < BIG_R; r++)
-            cnt += ((act >> r) & 1u) && (hk[r] >> BIG_CB) == (((unsigned long long)mhi << 32) | mlo);
-          cnt = __reduce_add_sync(0xffffffffu, cnt);
           const int buf = round & 1;
-          if (lane == 0) {
-            slot_k[buf * BIG_WARPS + warp] = wrow == 0x7fffffff ? 0ull : (((unsigned long long)mhi << 32) | mlo);
+          if (wrow != 0x7fffffff && brow == wrow) {  // the owner lane publishes value, row, column
+            slot_v[buf * BIG_WARPS + warp] = bv;
             slot_r[buf * BIG_WARPS + warp] = wrow;
-            slot_n[buf * BIG_WARPS + warp] = wrow == 0x7fffffff ? 0 : cnt;
+            slot_c[buf * BIG_WARPS + warp] = bcl;
+          } else if (wrow == 0x7fffffff && lane == 0) {
+            slot_r[buf * BIG_WARPS + warp] = 0x7fffffff;
           }
           __syncthreads();
           unsigned long long gv = 0ull;
-          int grow = 0x7fffffff, gcnt = 0;
+          int grow = 0x7fffffff, bcol = 0;
 #pragma unroll
           for (int w = 0; w < BIG_WARPS; w++) {
-            const unsigned long long v = slot_k[buf * BIG_WARPS + w];
             const int rw = slot_r[buf * BIG_WARPS + w];
             if (rw == 0x7fffffff) continue;
-            if (grow == 0x7fffffff || v > gv) { gv = v; grow = rw; gcnt = slot_n[buf * BIG_WARPS + w]; }
-            else if (v == gv) { grow = min(grow, rw); gcnt += slot_n[buf * BIG_WARPS + w]; }
-          }
-          if (shift > 0 && gcnt > 1) {
-            // several heads share the best truncated value: exact compare
-            // (X > 0, so the IEEE bits order the values)
-            unsigned long long bx = 0ull;
-            int br2 = 0x7fffffff;
-#pragma unroll
-            for (int r = 0; r < BIG_R; r++) {
-              const int i = tid + BIG_THREADS * r;
-              if (((act >> r) & 1u) && (hk[r] >> BIG_CB) == gv) {
-                const unsigned long long xb = big_bits(X[(size_t)i * N + big_key_col(hk[r])]);
-                if (br2 == 0x7fffffff || xb > bx) { bx = xb; br2 = i; }
-              }
-            }
-            const bool h2 = br2 != 0x7fffffff;
-            const unsigned x1 = (unsigned)(bx >> 32), x0 = (unsigned)bx;
-            const unsigned m1 = __reduce_max_sync(0xffffffffu, h2 ? x1 : 0u);
-            const unsigned m0 = __reduce_max_sync(0xffffffffu, (h2 && x1 == m1) ? x0 : 0u);
-            const bool c2 = h2 && x1 == m1 && x0 == m0;
-            const int r2 = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)br2 : 0x7fffffffu);
-            __syncthreads();  // slots of this buffer are read by everyone
-            if (lane == 0) {
-              slot_k[buf * BIG_WARPS + warp] = r2 == 0x7fffffff ? 0ull : (((unsigned long long)m1 << 32) | m0);
-              slot_r[buf * BIG_WARPS + warp] = r2;
-            }
-            __syncthreads();
-            gv = 0ull;
-            grow = 0x7fffffff;
-#pragma unroll
-            for (int w = 0; w < BIG_WARPS; w++) {
-              const unsigned long long v = slot_k[buf * BIG_WARPS + w];
-              const int rw = slot_r[buf * BIG_WARPS + w];
-              if (rw == 0x7fffffff) continue;
-              if (grow == 0x7fffffff || v > gv || (v == gv && rw < grow)) { gv = v; grow = rw; }
+            const unsigned long long v = slot_v[buf * BIG_WARPS + w];
+            if (grow == 0x7fffffff || v > gv || (v == gv && rw < grow)) {
+              gv = v;
+              grow = rw;
+              bcol = slot_c[buf * BIG_WARPS + w];
             }
           }
-          // winner: row grow, its head column (owner publishes it via the slot of round parity)
-          int bcol = 0;
-#pragma unroll
-          for (int r = 0; r < BIG_R; r++)
-            if (tid + BIG_THREADS * r == grow) bcol = big_key_col(hk[r]);
-          // the column is needed by everyone: broadcast through shared memory
-          int32_t *bc = slot_n + 2 * BIG_WARPS;
+          taken[bcol >> 5] |= 1u << (bcol & 31);  // every thread writes the same bit
           if ((grow & (BIG_THREADS - 1)) == tid) {
-            bc[buf] = bcol;
-            mrow[grow] = bcol;
-            taken[bcol >> 5] |= 1u << (bcol & 31);
             act &= ~(1u << (grow / BIG_THREADS));
+            mrow[grow] = bcol;
+            mval[grow] = gv;
           }
-          __syncthreads();
-          bcol = bc[buf];
           // advance rows whose head column was taken
 #pragma unroll
           for (int r = 0; r < BIG_R; r++) {
-            if (((act >> r) & 1u) && big_key_col(hk[r]) == bcol) {
+            if (((act >> r) & 1u) && hc[r] == bcol) {
               const int i = tid + BIG_THREADS * r;
-              int p = ptr[r] + 1;
-              unsigned long long kk = nk[r];
-              for (;;) {
-                const int col = big_key_col(kk);
-                if (!((taken[col >> 5] >> (col & 31)) & 1u)) break;
-                ++p;  // p < N: an active row always has an untaken column
-                kk = skey[(size_t)i * N + p];
-              }
-              hk[r] = kk;
+              int p = ptr[r];
+              int steps = 0;
+              do {  // p + 1 < N: an active row always has an untaken column
+                ++p;
+                ++steps;
+                hv[r] = qv[r][0];
+                hc[r] = qc[r][0];
+#pragma unroll
+                for (int f = 0; f + 1 < PF; f++) { qv[r][f] = qv[r][f + 1]; qc[r][f] = qc[r][f + 1]; }
+                if (p + PF < N) {
+                  qv[r][PF - 1] = sval[(size_t)i * N + p + PF];
+                  qc[r][PF - 1] = scol[(size_t)i * N + p + PF];
+                }
+              } while ((taken[hc[r] >> 5] >> (hc[r] & 31)) & 1u);
               ptr[r] = p;
-              if (p + 1 < N) nk[r] = skey[(size_t)i * N + p + 1];
+              if (prm.phase) {  // diagnostics: advances, advances past the prefetched window
+                atomicAdd(prm.phase + 5, (unsigned long long)steps);
+                if (steps > PF) atomicAdd(prm.phase + 6, 1ull);
+              }
             }
           }
         }
         __syncthreads();
         if (tid == 0) {  // similarity.py:150: Python sum in row order
           double wsum = 0.0;
-          for (int i = 0; i < N; i++) wsum += (double)X[(size_t)i * N + mrow[i]];
+          for (int i = 0; i < N; i++) wsum += (sizeof(T) == 8) ? __longlong_as_double((long long)mval[i])
+                                                               : (double)__uint_as_float((unsigned)mval[i]);
           if (out.d) out.d[slot] = isorank_distance_of(wsum, N);
           if (out.W) out.W[slot] = wsum;
           if (out.iters) out.iters[slot] = it_done;
@@ -919,6 +934,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         if (out.match)
           for (int i = tid; i < N; i += NT) out.match[i] = mrow[i];
       }
+      BIG_PHASE(5);
       if (out.X)
         for (int e = tid; e < N * N; e += NT) out.X[e] = (double)X[e];
       __syncthreads();
