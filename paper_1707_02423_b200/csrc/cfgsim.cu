@@ -554,8 +554,12 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
   DevCorpus dc = C->dev();
   T *useq = S.seq_u.as<T>();
   double *dseq = S.seq_d.as<double>();
+  // pass 0: typical list capacity; pass 1 re-runs only the combos that
+  // overflowed it (status 1) with dense-bound lists — decided on the device,
+  // so no host synchronisation sits between the stages
   for (int pass = 0; pass < 2; pass++) {
     sp.cap = pass == 0 ? 14 * kSeqNmax + 16 : kSeqNmax * kSeqNmax;
+    cb.redo = pass;
     const size_t smem = seq_smem_layout<T>(kSeqNmax, sp.cap).total;
     CU(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -565,18 +569,6 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
     void *args[] = {(void *)&dc, (void *)&cb, (void *)&sp, (void *)&useq, (void *)&dseq};
     CU(cudaLaunchKernel(f1, dim3((unsigned)grid), dim3(128), args, smem, st));
     g_launches++;
-    if (pass == 1) break;
-    std::vector<int32_t> stv(n);
-    CU(cudaMemcpyAsync(stv.data(), S.seq_st.as<int32_t>() + id0, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    std::vector<int64_t> redo;
-    for (int64_t q = 0; q < n; q++)
-      if (stv[q]) redo.push_back(id0 + q);
-    if (redo.empty()) break;
-    CU(grow_buf(S.seq_list, sizeof(int64_t) * redo.size(), st));
-    CU(cudaMemcpyAsync(S.seq_list.p, redo.data(), sizeof(int64_t) * redo.size(), cudaMemcpyHostToDevice, st));
-    cb.n = (int64_t)redo.size();
-    cb.list = S.seq_list.as<int64_t>();
   }
   return CFGSIM_OK;
 }
@@ -1333,9 +1325,12 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
     u = seg_end;
     a = a_end + 1;
   }
-  // overflowed / ambiguous pairs of all runs (records hold absolute units)
-  if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
-  if (int rc = big_status(S, st)) return rc;
+  // overflowed / ambiguous pairs of the per-pair kernels (records hold
+  // absolute units); the two-stage path alone needs no host round trip
+  if (u_end > u0) {
+    if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
+    if (int rc = big_status(S, st)) return rc;
+  }
   CU(cudaGetLastError());
   return CFGSIM_OK;
 }

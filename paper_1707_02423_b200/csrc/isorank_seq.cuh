@@ -44,6 +44,7 @@ struct SeqCombos {
   int64_t n;
   int64_t id0;          // combos id0 .. id0 + n - 1 (when list == NULL)
   const int64_t *list;  // else the combo ids to build
+  int32_t redo;         // 1: only combos whose status is 1 (dense-bound list re-run)
   const int32_t *g;
   const int32_t *nn;
   const int64_t *uoff;
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(64 * KB) isorank_seq_kernel(DevCorpus C, SeqCo
 
   for (int64_t ci = blockIdx.x; ci < cb.n; ci += gridDim.x) {
     const int64_t c = cb.list ? cb.list[ci] : cb.id0 + ci;
+    if (cb.redo && cb.status[c] == 0) continue;  // (uniform per CTA)
     const int g = cb.g[c], N = cb.nn[c];
     int32_t *nz = misc + 1;
     const bool ok = build_side<T, KB, 1, false>(C, g, N, N | 1, dense, lo_s, fr_s, zflag, zl, nz, toff, nullptr,
@@ -175,6 +177,7 @@ struct Pair2Params {
 // and sorts of the next pair.
 constexpr int P2_KC = 8;    // sweeps per staged chunk
 constexpr int P2_MW = 64;   // words of the ambiguous-sweep bitmask (kcap < 2048)
+constexpr int P2_KMAX = 512;  // kcap bound of the two-stage path (host checks)
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) {
@@ -187,7 +190,7 @@ struct P2Meta {
 };
 
 struct P2Smem {
-  size_t x[2], ord[2], meta, red, amb, item, first, mrow, total;
+  size_t x[2], ord[2], meta, red, amb, item, first, mrow, tab, total;
 };
 
 __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize) {
@@ -212,6 +215,7 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize) {
   s.item = take(sizeof(int64_t));
   s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
   s.mrow = take(sizeof(int32_t) * 192);
+  s.tab = take(sizeof(double) * 3 * (P2_KMAX + 2));  // alpha^m, (T)(c alpha^m), (T)(alpha^m / N^2)
   s.total = o;
   return s;
 }
@@ -569,6 +573,13 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   const double invN = 1.0 / (double)N;
   const double c = (1.0 - prm.alpha) * inv_nn;
   const int mmax = prm.max_iter < prm.kcap ? prm.max_iter : prm.kcap;
+  double *apw = (double *)(smem_raw + L.tab), *cfa = apw + (P2_KMAX + 2), *cfk = cfa + (P2_KMAX + 2);
+  for (int m = tid; m <= prm.kcap + 1; m += NP) {  // the per-pair coefficients, once per CTA
+    apw[m] = prm.apow[m];
+    cfa[m] = (double)(T)(c * prm.apow[m]);       // c alpha^m   (the low-rank kernel's cak)
+    cfk[m] = (double)(T)(prm.apow[m] * inv_nn);  // alpha^m/N^2 (its sc)
+  }
+  nbar_sync(BAR_P, NP);
   const int NPt = seq_pitch<T>(N);                      // history row pitch
   const int SPD = ((2 * NPt + 7) / 16) * 16 + 8;        // staged row pitch (== 8 mod 16 doubles: 2-wavefront fragments)
   for (int it = 0;; it++) {
@@ -610,14 +621,18 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     } else {
       // triangle unit -> sorted rows a <= b; the alignment runs in the caller's
       // (lower graph index, higher graph index) direction
+      // row a of unit uu: row_start[a] = a K - a (a - 1) / 2 <= uu, in closed form
       const int64_t uu = work.u0 + item;
-      int lo = 0, hi = work.K - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (work.row_start[mid] <= uu) lo = mid; else hi = mid - 1;
-      }
-      const int a = lo, b = a + (int)(uu - work.row_start[a]);
-      int pa = a, pb = b;
+      const int64_t Kt = work.K;
+      const double bq = 2.0 * (double)Kt + 1.0;
+      int64_t a = (int64_t)((bq - sqrt(bq * bq - 8.0 * (double)uu)) * 0.5);
+      auto rstart = [&](int64_t x) { return x * Kt - x * (x - 1) / 2; };
+      if (a < 0) a = 0;
+      if (a > Kt - 1) a = Kt - 1;
+      while (a > 0 && rstart(a) > uu) a--;
+      while (a + 1 < Kt && rstart(a + 1) <= uu) a++;
+      const int b = (int)(a + (uu - rstart(a)));
+      int pa = (int)a, pb = b;
       if (work.perm[pa] > work.perm[pb]) { const int t = pa; pa = pb; pb = t; }
       slot = uu - work.out_base;
       ca = prm.cbase + pa;
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     // then exact delta only for the ambiguous sweeps before the first
     // certain stop, in order
     for (int m = tid + 1; m <= mmax; m += NP) {
-      const double ak = prm.apow[m];
+      const double ak = apw[m];
       const double da = DA[m], db = DB[m];
       const double hiB = ak * invN * (da + db) * (1.0 + prm.eps);
       const double loB = ak * invN * fmax(da, db) * (1.0 - prm.eps);
@@ -668,7 +683,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
           double S = 0.0;
           for (int q = 0; q < PW; q++) S += red[q];
           nbar_sync(BAR_P, NP);  // red is rewritten by the next exact pass
-          if (prm.apow[m] * inv_nn * S < prm.tol) {  // similarity.py:144
+          if (apw[m] * inv_nn * S < prm.tol) {  // similarity.py:144
             K = m;
             conv = true;
             wd = P2_MW;
@@ -728,7 +743,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
         for (int k0 = 0; k0 < P2_KC; k0 += 4) {
           const int m = m0 + k0 + lk;  // this lane's k
           if (m0 + k0 > K) break;
-          const double cf = (m < K) ? (double)(T)(c * prm.apow[m]) : (m == K ? (double)(T)(prm.apow[K] * inv_nn) : 0.0);
+          const double cf = (m < K) ? cfa[m] : (m == K ? cfk[m] : 0.0);
           const double *row = buf + (k0 + lk) * SPD;
           double af[TR], bf[TC];
 #pragma unroll
@@ -821,7 +836,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
               for (int y = 0; y < BC; y++) vK[y] = vm[jj[y]];
               break;
             }
-            const T cak = (T)(c * prm.apow[m]);
+            const T cak = (T)cfa[m];
             T vb[BC];
 #pragma unroll
             for (int y = 0; y < BC; y++) vb[y] = vm[jj[y]];
@@ -836,7 +851,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
         nbar_sync(BAR_P, NP);  // buffer (ch & 1) is re-staged by chunk ch + 2 / X overwrites it
       }
       if (owner) {
-        const T sc = (T)(prm.apow[K] * inv_nn);
+        const T sc = (T)cfk[K];
 #pragma unroll
         for (int x = 0; x < AR; x++) {
           const T su = sc * uK[x];
