@@ -243,9 +243,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks (defaults = the production path): CFGSIM_BENCH_DEVICE pins every
+    # rank to one GPU and CFGSIM_BENCH_BACKEND=gloo replaces NCCL, so the N > 1
+    # code path can be exercised end to end on a one-GPU box
+    local = int(os.environ.get("CFGSIM_BENCH_DEVICE", local))
+    backend = os.environ.get("CFGSIM_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     cfg, mats, queries = corpus(args)
