@@ -45,6 +45,15 @@ extern "C" {
 #define CFGSIM_ERR_CUDA 3     /* CUDA runtime / launch failure                  */
 #define CFGSIM_ERR_NOMEM 4    /* device allocation failed                       */
 #define CFGSIM_ERR_NODEVICE 5 /* no usable sm_100 device: there is no CPU path  */
+#define CFGSIM_ERR_DEGENERATE 6 /* measure undefined (reference: DegenerateInput) */
+#define CFGSIM_ERR_ORDER 7    /* Minkowski order p < 1 (reference: BadOrder)    */
+
+/* flat measures (similarity.py:20-66) */
+#define CFGSIM_EUC 0
+#define CFGSIM_MAN 1
+#define CFGSIM_MIN 2
+#define CFGSIM_JAC 3
+#define CFGSIM_COS 4
 
 #define CFGSIM_FP64 0
 #define CFGSIM_FP32 1
@@ -135,6 +144,20 @@ CFGSIM_API int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, in
  * src n x n, dst target x target, dense row-major host arrays. */
 CFGSIM_API int cfgsim_interpolate(int32_t device, int32_t n, const double *src, int32_t target,
                        double *dst);
+
+/* Flat measures after normalize_pair: measure_distance(a, b, EUC|MAN|MIN|JAC|COS,
+ * p) (similarity.py:29-66,176-200).  cfgsim_flat_single: dense host inputs;
+ * returns CFGSIM_ERR_DEGENERATE where jaccard / cosine are undefined and
+ * CFGSIM_ERR_ORDER for minkowski with p < 1.  cfgsim_flat_pairs: batched over
+ * two corpora, NaN where undefined.  cfgsim_flat_allpairs: pairwise(...) for a
+ * flat measure (similarity.py:247-255): symmetric K x K in the caller's graph
+ * order, zero diagonal, NaN for undefined pairs.  [host|device] outputs. */
+CFGSIM_API int cfgsim_flat_single(int32_t device, int32_t na, const double *A, int32_t nb, const double *B,
+                                  int32_t measure, double p, double *out);
+CFGSIM_API int cfgsim_flat_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_pairs, const int32_t *ia,
+                                 const int32_t *ib, int32_t measure, double p, double *out, void *cuda_stream);
+CFGSIM_API int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, double p, double *d_mat,
+                                    void *cuda_stream);
 
 /* Number of pair-kernel launches issued by this process so far (bench
  * evidence for gpu_launches). */

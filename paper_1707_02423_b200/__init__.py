@@ -2,8 +2,10 @@
 
 Public surface mirrors ``pkg/src/sasscfg/__init__.py:41-54`` for the hot
 path: ``isorank_align``, ``isorank_distance``, ``measure_distance``,
-``pairwise``, ``minmax_scale``, ``export_heatmap_csv`` plus the types they
-use; ``nearest`` and ``isorank_pairs`` are new batched entry points.
+``pairwise``, ``minmax_scale``, ``export_heatmap_csv``, the flat measures
+(``euclidean``, ``manhattan``, ``minkowski``, ``jaccard``, ``cosine``) plus
+the types they use; ``nearest`` and ``isorank_pairs`` are new batched entry
+points.
 """
 
 from .errors import (BadOrder, BadTarget, DegenerateInput, DeviceError, DimMismatch, DuplicateKernel,
@@ -11,8 +13,9 @@ from .errors import (BadOrder, BadTarget, DegenerateInput, DeviceError, DimMisma
 from .matrix import (GLOBAL, INTERPOLATED, RAW_COUNTS, ROW_STOCHASTIC, TransitionMatrix, interpolate_to,
                      normalize_pair)
 from .corpus import DeviceCorpus, pack
-from .similarity import (AlignmentResult, MeasureId, PairwiseMatrix, export_heatmap_csv, isorank_align,
-                         isorank_distance, isorank_pairs, measure_distance, minmax_scale, nearest, pairwise)
+from .similarity import (AlignmentResult, MeasureId, PairwiseMatrix, cosine, euclidean, export_heatmap_csv,
+                         isorank_align, isorank_distance, isorank_pairs, jaccard, manhattan, measure_distance,
+                         minkowski, minmax_scale, nearest, pairwise)
 
 __version__ = "0.1.0"
 
@@ -22,4 +25,5 @@ __all__ = [
     "PairwiseMatrix", "RAW_COUNTS", "ROW_STOCHASTIC", "SasscfgError", "TransitionMatrix",
     "export_heatmap_csv", "interpolate_to", "isorank_align", "isorank_distance", "isorank_pairs",
     "measure_distance", "minmax_scale", "nearest", "normalize_pair", "pack", "pairwise",
+    "euclidean", "manhattan", "minkowski", "jaccard", "cosine",
 ]

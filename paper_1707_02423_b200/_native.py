@@ -14,11 +14,12 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import DeviceError, DimMismatch
+from .errors import BadOrder, DegenerateInput, DeviceError, DimMismatch
 
 LIB_PATH = Path(__file__).resolve().parent / "libcfgsim.so"
 
-OK, ERR_ARG, ERR_DIM, ERR_CUDA, ERR_NOMEM, ERR_NODEVICE = range(6)
+OK, ERR_ARG, ERR_DIM, ERR_CUDA, ERR_NOMEM, ERR_NODEVICE, ERR_DEGENERATE, ERR_ORDER = range(8)
+FLAT_IDS = {"euc": 0, "man": 1, "min": 2, "jac": 3, "cos": 4}
 FP64, FP32 = 0, 1
 
 if not LIB_PATH.exists():
@@ -57,6 +58,9 @@ _SIGS = {
                               C.c_int),
     "cfgsim_nearest": ([_vp, _vp, _i32, _i32, _pp, _vp, _vp, _vp], C.c_int),
     "cfgsim_interpolate": ([_i32, _i32, _vp, _i32, _vp], C.c_int),
+    "cfgsim_flat_single": ([_i32, _i32, _vp, _i32, _vp, _i32, C.c_double, _vp], C.c_int),
+    "cfgsim_flat_pairs": ([_vp, _vp, _i64, _vp, _vp, _i32, C.c_double, _vp, _vp], C.c_int),
+    "cfgsim_flat_allpairs": ([_vp, _i32, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_launch_count": ([], C.c_int64),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -77,6 +81,10 @@ def check(rc: int) -> None:
         raise DimMismatch(msg)
     if rc == ERR_NOMEM:
         raise MemoryError(msg)
+    if rc == ERR_DEGENERATE:
+        raise DegenerateInput(msg)
+    if rc == ERR_ORDER:
+        raise BadOrder(msg)
     raise DeviceError(msg)
 
 

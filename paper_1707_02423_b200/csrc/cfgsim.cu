@@ -23,6 +23,7 @@
 #include "isorank.cuh"
 #include "tiers.h"
 #include "isorank_lr.cuh"
+#include "flat.cuh"
 
 using namespace cfgsim;
 
@@ -1055,6 +1056,33 @@ int corpus_from_dense(int device, int n, const double *M, cfgsim_corpus **out) {
 
 }  // namespace
 
+namespace {
+// Flat-measure launch over a pair list or the upper triangle of one corpus.
+int flat_launch(const cfgsim_corpus *A, const cfgsim_corpus *B, FlatWork w, double *out, cudaStream_t st) {
+  if (w.n_items <= 0) return CFGSIM_OK;
+  w.nlim = std::max(A->max_nodes, B->max_nodes);
+  const size_t smem = sizeof(double) * 4 * (size_t)w.nlim;
+  if (smem > kMaxSmem) return fail(CFGSIM_ERR_ARG, "flat measures: graph too large for the row buffers");
+  CU(cudaFuncSetAttribute((const void *)flat_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev, sms = 0, occ = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)flat_pair_kernel, FLAT_THREADS, smem));
+  const int64_t grid = std::min<int64_t>((int64_t)sms * std::max(occ, 1), w.n_items);
+  flat_pair_kernel<<<(unsigned)grid, FLAT_THREADS, smem, st>>>(A->dev(), B->dev(), w, out);
+  g_launches++;
+  CU(cudaGetLastError());
+  return CFGSIM_OK;
+}
+
+int check_flat(int32_t measure, double p) {
+  if (measure < CFGSIM_EUC || measure > CFGSIM_COS) return fail(CFGSIM_ERR_ARG, "unknown flat measure");
+  if (measure == CFGSIM_MIN && !(p >= 1.0))
+    return fail(CFGSIM_ERR_ORDER, "order p must be >= 1");  // similarity.py:46-47 (BadOrder)
+  return CFGSIM_OK;
+}
+}  // namespace
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -1596,6 +1624,88 @@ int cfgsim_interpolate(int32_t device, int32_t n, const double *src, int32_t tar
   interp_kernel<<<(target * target + 255) / 256, 256>>>(n, s.as<double>(), target, d.as<double>());
   CU(cudaGetLastError());
   CU(cudaMemcpy(dst, d.p, sizeof(double) * target * target, cudaMemcpyDeviceToHost));
+  return CFGSIM_OK;
+}
+
+int cfgsim_flat_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_pairs, const int32_t *ia,
+                      const int32_t *ib, int32_t measure, double p, double *out, void *cuda_stream) {
+  if (!A || !B || n_pairs < 0 || (n_pairs && (!ia || !ib || !out))) return fail(CFGSIM_ERR_ARG, "bad pair arguments");
+  if (A->device != B->device) return fail(CFGSIM_ERR_ARG, "corpora live on different devices");
+  if (int rc = set_device(A->device)) return rc;
+  const bool bad_order = measure == CFGSIM_MIN && !(p >= 1.0);
+  if (!bad_order)
+    if (int rc = check_flat(measure, p)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  std::vector<int32_t> ha(n_pairs), hb(n_pairs);
+  if (n_pairs) {
+    CU(cudaMemcpyAsync(ha.data(), ia, sizeof(int32_t) * n_pairs, cudaMemcpyDefault, st));
+    CU(cudaMemcpyAsync(hb.data(), ib, sizeof(int32_t) * n_pairs, cudaMemcpyDefault, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  for (int64_t q = 0; q < n_pairs; q++)
+    if (ha[q] < 0 || ha[q] >= A->K || hb[q] < 0 || hb[q] >= B->K) return fail(CFGSIM_ERR_ARG, "pair index out of range");
+  DBuf dia, dib;
+  CU(dia.alloc(sizeof(int32_t) * std::max<int64_t>(n_pairs, 1)));
+  CU(dib.alloc(sizeof(int32_t) * std::max<int64_t>(n_pairs, 1)));
+  CU(cudaMemcpyAsync(dia.p, ha.data(), sizeof(int32_t) * n_pairs, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dib.p, hb.data(), sizeof(int32_t) * n_pairs, cudaMemcpyHostToDevice, st));
+  OutStage so;
+  CU(so.prepare(out, sizeof(double) * n_pairs));
+  FlatWork w{};
+  w.mode = 0;
+  w.n_items = n_pairs;
+  w.ia = dia.as<int32_t>();
+  w.ib = dib.as<int32_t>();
+  w.measure = measure;
+  w.p = p;
+  if (int rc = flat_launch(A, B, w, (double *)so.dev, st)) return rc;
+  CU(so.finish(st));
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, double p, double *d_mat, void *cuda_stream) {
+  if (!c || !d_mat) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  if (int rc = set_device(c->device)) return rc;
+  const bool bad_order = measure == CFGSIM_MIN && !(p >= 1.0);
+  if (!bad_order)
+    if (int rc = check_flat(measure, p)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t KK = (size_t)c->K * c->K;
+  OutStage so;
+  CU(so.prepare(d_mat, sizeof(double) * KK));
+  CU(cudaMemsetAsync(so.dev, 0, sizeof(double) * KK, st));  // definitional zero diagonal (similarity.py:248-255)
+  FlatWork w{};
+  w.mode = 1;
+  w.n_items = (int64_t)c->K * (c->K - 1) / 2;
+  w.K = c->K;
+  w.measure = measure;
+  w.p = p;  // p < 1: every pair is NaN (BadOrder caught per pair, :243-246)
+  if (int rc = flat_launch(c, c, w, (double *)so.dev, st)) return rc;
+  CU(so.finish(st));
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+int cfgsim_flat_single(int32_t device, int32_t na, const double *A, int32_t nb, const double *B, int32_t measure,
+                       double p, double *out) {
+  if (na < 1 || nb < 1 || !A || !B || !out) return fail(CFGSIM_ERR_ARG, "bad matrices");
+  if (int rc = check_flat(measure, p)) return rc;
+  if (int rc = set_device(device)) return rc;
+  cfgsim_corpus *ca = nullptr, *cb = nullptr;
+  if (int rc = corpus_from_dense(device, na, A, &ca)) return rc;
+  if (int rc = corpus_from_dense(device, nb, B, &cb)) {
+    cfgsim_corpus_destroy(ca);
+    return rc;
+  }
+  const int32_t zero = 0;
+  int rc = cfgsim_flat_pairs(ca, cb, 1, &zero, &zero, measure, p, out, nullptr);
+  cfgsim_corpus_destroy(ca);
+  cfgsim_corpus_destroy(cb);
+  if (rc) return rc;
+  if (std::isnan(*out)) return fail(CFGSIM_ERR_DEGENERATE, measure == CFGSIM_JAC
+                                                             ? "jaccard undefined for two all-zero matrices"
+                                                             : "cosine undefined for an all-zero matrix");
   return CFGSIM_OK;
 }
 

@@ -13,8 +13,10 @@ Additions (keyword-only, defaults reproduce the reference):
   device=None               GPU ordinal (default: LOCAL_RANK or 0)
 and ``nearest`` (query-vs-corpus best match, no reference equivalent).
 
-The five flat measures (euc/man/min/jac/cos) are outside this round's hot
-path and raise NotImplementedError here.
+The five flat measures (euc/man/min/jac/cos, similarity.py:29-66) run on the
+GPU too (``csrc/flat.cuh``): same values up to summation
+order, same errors (DimMismatch, BadOrder, DegenerateInput; NaN inside
+``pairwise``).
 """
 
 from __future__ import annotations
@@ -27,7 +29,7 @@ import numpy as np
 
 from . import _native as nat
 from .corpus import DeviceCorpus, pack
-from .errors import DegenerateInput, DimMismatch, DuplicateKernel
+from .errors import BadOrder, DegenerateInput, DimMismatch, DuplicateKernel
 from .matrix import TransitionMatrix
 
 
@@ -66,6 +68,53 @@ def _dev(device):
 def _check_alpha(alpha: float) -> None:
     if not 0.0 < alpha < 1.0:  # similarity.py:129-130
         raise ValueError(f"alpha must be in (0, 1), got {alpha}")
+
+
+def _flat(a: TransitionMatrix, b: TransitionMatrix, measure: str, p: float = 3.0, device=None) -> float:
+    """One flat measure on the GPU after normalize_pair (measure_distance's order)."""
+    A = np.ascontiguousarray(a.entries, dtype=np.float64)
+    B = np.ascontiguousarray(b.entries, dtype=np.float64)
+    out = np.empty(1)
+    nat.check(nat.lib.cfgsim_flat_single(_dev(device), a.n, nat.ptr(A), b.n, nat.ptr(B), nat.FLAT_IDS[measure],
+                                         float(p), nat.ptr(out)))
+    return float(out[0])
+
+
+def _same_size(a: TransitionMatrix, b: TransitionMatrix) -> None:
+    if a.n != b.n:  # similarity.py:29-32
+        raise DimMismatch(f"matrix dimensions differ: {a.n} vs {b.n}")
+
+
+def euclidean(a: TransitionMatrix, b: TransitionMatrix) -> float:
+    """``sqrt(sum |x - y|^2)`` over the flattened entries (similarity.py:35-37)."""
+    _same_size(a, b)
+    return _flat(a, b, "euc")
+
+
+def manhattan(a: TransitionMatrix, b: TransitionMatrix) -> float:
+    """``sum |x - y|`` (similarity.py:40-42)."""
+    _same_size(a, b)
+    return _flat(a, b, "man")
+
+
+def minkowski(a: TransitionMatrix, b: TransitionMatrix, p: float = 3.0) -> float:
+    """``(sum |x - y|^p)^(1/p)``, p >= 1 else BadOrder (similarity.py:45-49)."""
+    if p < 1:
+        raise BadOrder(f"order p must be >= 1, got {p}")
+    _same_size(a, b)
+    return _flat(a, b, "min", p)
+
+
+def jaccard(a: TransitionMatrix, b: TransitionMatrix) -> float:
+    """``sum (x-y)^2 / (x.x + y.y - x.y)``; DegenerateInput for two zero matrices (similarity.py:52-57)."""
+    _same_size(a, b)
+    return _flat(a, b, "jac")
+
+
+def cosine(a: TransitionMatrix, b: TransitionMatrix) -> float:
+    """``1 - x.y / (|x| |y|)``; DegenerateInput for a zero matrix (similarity.py:60-66)."""
+    _same_size(a, b)
+    return _flat(a, b, "cos")
 
 
 def isorank_align(a: TransitionMatrix, b: TransitionMatrix, alpha: float = 0.85, tol: float = 1e-9,
@@ -115,9 +164,11 @@ def measure_distance(a: TransitionMatrix, b: TransitionMatrix, measure: MeasureI
     For ISO the size normalisation (``normalize_pair``) is fused into the
     kernel prologue."""
     if measure is not MeasureId.ISO:
-        if measure in tuple(MeasureId):
-            raise NotImplementedError(f"measure {measure.value!r} is not on this build's hot path")
-        raise ValueError(f"unknown measure {measure!r}")
+        if measure not in tuple(MeasureId):
+            raise ValueError(f"unknown measure {measure!r}")
+        if measure is MeasureId.MIN and p < 1:
+            raise BadOrder(f"order p must be >= 1, got {p}")
+        return _flat(a, b, measure.value, p, device)  # normalize_pair fused (similarity.py:187-199)
     _check_alpha(alpha)
     A = np.ascontiguousarray(a.entries, dtype=np.float64)
     B = np.ascontiguousarray(b.entries, dtype=np.float64)
@@ -141,12 +192,18 @@ def pairwise(matrices: list[TransitionMatrix], measure: MeasureId, *, p: float =
     ids = tuple(m.kernel_id for m in ordered)
     if len(set(ids)) != len(ids):
         raise DuplicateKernel("duplicate kernel_id in pairwise input")
-    if measure is not MeasureId.ISO:
-        if measure in tuple(MeasureId):
-            raise NotImplementedError(f"measure {measure.value!r} is not on this build's hot path")
+    if measure not in tuple(MeasureId):
         raise ValueError(f"unknown measure {measure!r}")
-    _check_alpha(alpha)
     k = len(ordered)
+    if measure is not MeasureId.ISO:
+        # symmetric, zero diagonal, NaN where the measure fails (similarity.py:247-255)
+        scores = np.empty((k, k))
+        with DeviceCorpus(pack(ordered), _dev(device)) as corpus:
+            nat.check(nat.lib.cfgsim_flat_allpairs(corpus.handle, nat.FLAT_IDS[measure.value], float(p),
+                                                   nat.ptr(scores), None))
+        pm = PairwiseMatrix(measure=measure, kernel_ids=ids, scores=scores, scaled=False)
+        return (pm, None) if return_iterations else pm
+    _check_alpha(alpha)
     scores = np.empty((k, k))
     iters = np.empty((k, k), np.int32) if return_iterations else None
     prm = nat.params(alpha, tol, max_iter, precision)
