@@ -458,6 +458,81 @@ __device__ __forceinline__ void p2_row_order(const unsigned long long *Krow, int
   }
 }
 
+// Same order for 32 < N <= 64 with two threads per row (adjacent lanes: half 0
+// sorts positions 0..31 descending, half 1 positions 32..63 ascending; a
+// shuffle exchange makes both halves bitonic, an in-register merge finishes).
+template <typename T>
+__device__ __forceinline__ void p2_row_order_pair(const unsigned long long *Krow, int N, uint8_t *ord, int half,
+                                                  bool act) {
+  constexpr int VB = sizeof(T) == 8 ? 58 : 31;
+  uint32_t v[32];
+#pragma unroll
+  for (int q = 0; q < 32; q++) {
+    const int j = half * 32 + q;
+    v[q] = (act && j < N) ? (uint32_t)((((Krow[j] >> 6) >> (VB - 26)) << 6) | (Krow[j] & 63ull)) : 0u;
+  }
+  // sort half 0 descending, half 1 ascending (padding 0 ends up last overall)
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t a = v[i], b = v[l];
+          const uint32_t hi = max(a, b), lo = min(a, b);
+          const bool desc = ((i & k) == 0) == (half == 0);
+          v[i] = desc ? hi : lo;
+          v[l] = desc ? lo : hi;
+        }
+      }
+#pragma unroll
+  for (int q = 0; q < 32; q++) {  // half 0 keeps the larger 32, half 1 the smaller
+    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[q], 1);
+    v[q] = half == 0 ? max(v[q], o) : min(v[q], o);
+  }
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1)
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      const int l = i ^ j;
+      if (l > i) {
+        const uint32_t a = v[i], b = v[l];
+        v[i] = max(a, b);
+        v[l] = min(a, b);
+      }
+    }
+  bool coll = false;
+#pragma unroll
+  for (int q = 0; q < 32; q++) {
+    const int pos = half * 32 + q;
+    if (act && pos < N) ord[pos] = (uint8_t)(63 - (int)(v[q] & 63u));
+    if (q + 1 < 32 && act && pos + 1 < N && (v[q] >> 6) == (v[q + 1] >> 6) &&
+        (Krow[63 - (v[q] & 63u)] >> 6) != (Krow[63 - (v[q + 1] & 63u)] >> 6))
+      coll = true;
+  }
+  const uint32_t first1 = __shfl_down_sync(0xffffffffu, v[0], 1);  // half 1's first, seen by half 0
+  if (half == 0 && act && 32 < N && (v[31] >> 6) == (first1 >> 6) &&
+      (Krow[63 - (v[31] & 63u)] >> 6) != (Krow[63 - (first1 & 63u)] >> 6))
+    coll = true;
+  const int other = __shfl_xor_sync(0xffffffffu, coll ? 1 : 0, 1);  // (unconditional: every lane shuffles)
+  coll = coll || other != 0;
+  __syncwarp();
+  if (coll && half == 0) {  // rare: exact insertion pass over the whole row
+    for (int p = 1; p < N; p++) {
+      const uint8_t cp = ord[p];
+      const unsigned long long kp = Krow[cp];
+      int q = p - 1;
+      while (q >= 0 && Krow[ord[q]] < kp) {
+        ord[q + 1] = ord[q];
+        q--;
+      }
+      ord[q + 1] = cp;
+    }
+  }
+}
+
 // Greedy rounds on sorted key rows (pitch PK), one warp: a head's cross-row
 // key swaps the column field for (63 - row), so one 64-bit max picks the best
 // head with ties to the lowest row — np.argmax's first occurrence.
@@ -895,7 +970,13 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     unsigned long long *Kr = (unsigned long long *)Xs;
     if (keys) {
       // ---- row orders: one thread per row, 32-bit prefix keys in registers
-      if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * N);
+      if constexpr (KB == 2) {  // two adjacent lanes per row
+        const int row = tid >> 1, half = tid & 1;
+        const bool act = row < N;
+        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * N, half, act);
+      } else {
+        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * N);
+      }
     } else {
       for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * N, lane);
     }
