@@ -176,7 +176,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, FileNotFoundError):
             self.proc = None
         time.sleep(0.3)
@@ -360,7 +360,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     launches = nat.launch_count() - launches0
-    t_step = sum(e[0].elapsed_time(e[2]) for e in evs) / 1e3
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    t_step = sum(step_ms) / 1e3
     t_kern = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
     tt = torch.tensor([t_step, t_kern, rank_flops, tp_flops], dtype=torch.float64, device=dev)
     if world > 1:
@@ -446,6 +447,7 @@ def run_ours(args):
                              "note": "SURVEY 8(d) F = sum_iters [2N(S_A+S_B) + N(z_A+z_B) + 8N^2]: the reference "
                                      "iteration's work; the closed form executes far less, so this exceeds 1"}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "step_ms": [round(x, 3) for x in step_ms],
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -559,16 +559,21 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
   // overflowed it (status 1) with dense-bound lists — decided on the device,
   // so no host synchronisation sits between the stages
   for (int pass = 0; pass < 2; pass++) {
-    sp.cap = pass == 0 ? 14 * kSeqNmax + 16 : kSeqNmax * kSeqNmax;
+    // pass 0: four combos per CTA, warp-synchronous recurrences; pass 1: the
+    // one-combo-per-CTA kernel re-runs flagged combos with dense-bound lists
+    sp.cap = pass == 0 ? 10 * kSeqNmax + 16 : kSeqNmax * kSeqNmax;  // 10N+16: 2 CTAs/SM
     cb.redo = pass;
-    const size_t smem = seq_smem_layout<T>(kSeqNmax, sp.cap).total;
-    CU(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const void *fk = pass == 0 ? (const void *)isorank_seq4_kernel<T, 2> : f1;
+    const int nthr = pass == 0 ? 32 * SEQ4 : 128;
+    const size_t smem = pass == 0 ? seq4_smem_layout<T>(kSeqNmax, sp.cap).total : seq_smem_layout<T>(kSeqNmax, sp.cap).total;
+    CU(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f1, 128, smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fk, nthr, smem));
     if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-1 kernel cannot be resident");
-    const int64_t grid = std::min<int64_t>((int64_t)sms * occ, cb.n);
+    const int64_t units = pass == 0 ? (cb.n + SEQ4 - 1) / SEQ4 : cb.n;
+    const int64_t grid = std::min<int64_t>((int64_t)sms * occ, units);
     void *args[] = {(void *)&dc, (void *)&cb, (void *)&sp, (void *)&useq, (void *)&dseq};
-    CU(cudaLaunchKernel(f1, dim3((unsigned)grid), dim3(128), args, smem, st));
+    CU(cudaLaunchKernel(fk, dim3((unsigned)grid), dim3(nthr), args, smem, st));
     g_launches++;
   }
   return CFGSIM_OK;

@@ -154,6 +154,151 @@ __global__ void __launch_bounds__(64 * KB) isorank_seq_kernel(DevCorpus C, SeqCo
   }
 }
 
+// Stage 1, four combos per CTA: the CTA builds the four operators one after
+// the other (build_side needs the whole CTA and the dense scratch), then each
+// warp runs one combo's recurrence warp-synchronously (no CTA barrier per
+// sweep).  Same arithmetic as isorank_seq_kernel (lr_matvec_entry, same
+// lists), so the u histories are bitwise identical.  Combos whose lists
+// overflow are flagged for the one-per-CTA kernel's dense re-run.
+constexpr int SEQ4 = 8;  // combos (= warps) per CTA
+
+struct Seq4Smem {
+  size_t dense, idx, w, toff, z, nz, u, lo, fr, zflag, misc, total;
+};
+
+template <typename T>
+__host__ __device__ inline Seq4Smem seq4_smem_layout(int nlim, int cap) {
+  Seq4Smem s;
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o += (b + 15) & ~size_t(15);
+    return at;
+  };
+  s.dense = take(sizeof(double) * (size_t)nlim * (nlim | 1));
+  s.idx = take(sizeof(int32_t) * (size_t)cap * SEQ4);
+  s.w = take(sizeof(T) * (size_t)cap * SEQ4);
+  s.toff = take(sizeof(int32_t) * (nlim + 1) * SEQ4);
+  s.z = take(sizeof(int32_t) * (nlim + 1) * SEQ4);
+  s.nz = take(sizeof(int32_t) * 4 * SEQ4);
+  s.u = take(sizeof(T) * 2 * nlim * SEQ4);
+  s.lo = take(sizeof(int32_t) * (nlim + 1));
+  s.fr = take(sizeof(double) * (nlim + 1));
+  s.zflag = take(sizeof(uint8_t) * (nlim + 1));
+  s.misc = take(64);
+  s.total = o;
+  return s;
+}
+
+template <typename T, int KB>
+__global__ void __launch_bounds__(32 * SEQ4) isorank_seq4_kernel(DevCorpus C, SeqCombos cb, SeqParams prm, T *useq,
+                                                                double *dseq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Seq4Smem L = seq4_smem_layout<T>(prm.nlim, prm.cap);
+  double *dense = (double *)(smem_raw + L.dense);
+  int32_t *lo_s = (int32_t *)(smem_raw + L.lo);
+  double *fr_s = (double *)(smem_raw + L.fr);
+  uint8_t *zflag = (uint8_t *)(smem_raw + L.zflag);
+  int32_t *misc = (int32_t *)(smem_raw + L.misc);
+  int32_t *nzs = (int32_t *)(smem_raw + L.nz);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nl = prm.nlim;
+  for (int64_t g0 = (int64_t)blockIdx.x * SEQ4; g0 < cb.n; g0 += (int64_t)gridDim.x * SEQ4) {
+    // ---- build up to four operators (whole CTA), lists in slot s
+    for (int s = 0; s < SEQ4 && g0 + s < cb.n; s++) {
+      const int64_t c = cb.id0 + g0 + s;
+      int32_t *idx = (int32_t *)(smem_raw + L.idx) + (size_t)s * prm.cap;
+      T *w = (T *)(smem_raw + L.w) + (size_t)s * prm.cap;
+      int32_t *toff = (int32_t *)(smem_raw + L.toff) + s * (nl + 1);
+      int32_t *zl = (int32_t *)(smem_raw + L.z) + s * (nl + 1);
+      const bool ok = build_side<T, KB, 1, false>(C, cb.g[c], cb.nn[c], cb.nn[c] | 1, dense, lo_s, fr_s, zflag, zl,
+                                                  nzs + 4 * s, toff, nullptr, idx, w, prm.cap, false, misc);
+      if (tid == 0) {
+        nzs[4 * s + 1] = ok ? 1 : 0;
+        cb.status[c] = ok ? 0 : 1;
+      }
+      __syncthreads();
+    }
+    // ---- warp s: recurrence of combo g0 + s
+    if (g0 + warp < cb.n && nzs[4 * warp + 1]) {
+      const int64_t c = cb.id0 + g0 + warp;
+      const int N = cb.nn[c];
+      const int32_t *idx = (const int32_t *)(smem_raw + L.idx) + (size_t)warp * prm.cap;
+      const T *w = (const T *)(smem_raw + L.w) + (size_t)warp * prm.cap;
+      const int32_t *toff = (const int32_t *)(smem_raw + L.toff) + warp * (nl + 1);
+      const int32_t *zl = (const int32_t *)(smem_raw + L.z) + warp * (nl + 1);
+      const int nzv = nzs[4 * warp];
+      T *u = (T *)(smem_raw + L.u) + (size_t)warp * 2 * nl;
+      const T invN = (T)(1.0 / (double)N);
+      const int NPt = seq_pitch<T>(N);
+      T *U = useq + cb.uoff[c];
+      double *D = dseq + c * (int64_t)(prm.kcap + 1);
+      for (int t = lane; t < N; t += 32) {
+        u[t] = (T)1;
+        U[t] = (T)1;
+      }
+      if (lane == 0) D[0] = 0.0;
+      __syncwarp();
+      for (int m = 1; m <= prm.kcap; m++) {
+        const T *uo = u + ((m - 1) & 1) * nl;
+        T *un = u + (m & 1) * nl;
+        // lr_matvec_entry with the uniform-row term hoisted (computed once per
+        // lane, same operation order) and the lane's two outputs interleaved
+        T z0 = 0, z1 = 0;
+        {
+          int e = 0;
+          for (; e + 1 < nzv; e += 2) {
+            z0 += uo[zl[e]];
+            z1 += uo[zl[e + 1]];
+          }
+          if (e < nzv) z0 += uo[zl[e]];
+        }
+        const T zt = (z0 + z1) * invN;
+        const int t0 = lane, t1 = lane + 32;
+        T a0 = zt, a1 = 0, b0 = zt, b1 = 0;
+        {
+          int e = toff[t0], e1 = t0 < N ? toff[t0 + 1] : e;
+          int f = t1 < N ? toff[t1] : 0, f1 = t1 < N ? toff[t1 + 1] : 0;
+          while (e + 1 < e1 || f + 1 < f1) {
+            if (e + 1 < e1) {
+              a0 = fma(w[e], uo[idx[e]], a0);
+              a1 = fma(w[e + 1], uo[idx[e + 1]], a1);
+              e += 2;
+            }
+            if (f + 1 < f1) {
+              b0 = fma(w[f], uo[idx[f]], b0);
+              b1 = fma(w[f + 1], uo[idx[f + 1]], b1);
+              f += 2;
+            }
+          }
+          if (e < e1) a0 = fma(w[e], uo[idx[e]], a0);
+          if (f < f1) b0 = fma(w[f], uo[idx[f]], b0);
+        }
+        double part = 0.0;
+        if (t0 < N) {
+          const T v = a0 + a1;
+          un[t0] = v;
+          U[(size_t)m * NPt + t0] = v;
+          part += fabs((double)v - (double)uo[t0]);
+        }
+        if (t1 < N) {
+          const T v = b0 + b1;
+          un[t1] = v;
+          U[(size_t)m * NPt + t1] = v;
+          part += fabs((double)v - (double)uo[t1]);
+        }
+        // (fixed order; may differ from the CTA kernel's D in the last bits —
+        // D only feeds the bracket, whose 1e-6 margin makes K independent of it)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) D[m] = part;
+        __syncwarp();
+      }
+    }
+    __syncthreads();  // lists / rings are rebuilt for the next group
+  }
+}
+
 // Stage 2 work: the all-pairs triangle in size-sorted order, restricted to
 // rows of one N; combo of sorted position b for this N = cbase + b.
 struct Pair2Params {

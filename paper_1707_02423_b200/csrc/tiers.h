@@ -65,6 +65,10 @@ extern template __global__ void cfgsim::isorank_seq_kernel<double, 2>(cfgsim::De
                                                                       cfgsim::SeqParams, double *, double *);
 extern template __global__ void cfgsim::isorank_seq_kernel<float, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos,
                                                                      cfgsim::SeqParams, float *, double *);
+extern template __global__ void cfgsim::isorank_seq4_kernel<double, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos,
+                                                                       cfgsim::SeqParams, double *, double *);
+extern template __global__ void cfgsim::isorank_seq4_kernel<float, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos,
+                                                                      cfgsim::SeqParams, float *, double *);
 CFGSIM_BIG_LIST_T(double, CFGSIM_EXTERN_BIG)
 CFGSIM_BIG_LIST_T(float, CFGSIM_EXTERN_BIG)
 CFGSIM_TIER_LIST(CFGSIM_EXTERN_TIER)

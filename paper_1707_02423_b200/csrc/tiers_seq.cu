@@ -11,3 +11,7 @@ template __global__ void cfgsim::isorank_seq_kernel<float, 2>(cfgsim::DevCorpus,
       const int32_t *, cfgsim::PairWork, cfgsim::PairOut, cfgsim::Pair2Params, const T *, const double *, \
       const int64_t *, unsigned long long *);
 CFGSIM_P2_LIST(CFGSIM_P2)
+template __global__ void cfgsim::isorank_seq4_kernel<double, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos, cfgsim::SeqParams,
+                                                                double *, double *);
+template __global__ void cfgsim::isorank_seq4_kernel<float, 2>(cfgsim::DevCorpus, cfgsim::SeqCombos, cfgsim::SeqParams,
+                                                               float *, double *);
