@@ -400,10 +400,10 @@ def run_ours(args):
             res = call()
             times.append(time.perf_counter() - t0)
         if args.config == "c3":
-            h2d = int(P.corpus.packed_bytes(P.pack(queries)) + P.corpus.packed_bytes(P.pack(mats)))
+            h2d = int(q_d.h2d_bytes + corpus_d.h2d_bytes)  # corpus uploads (CSR + CSC + tables)
             d2h = int(res[0].nbytes + res[1].nbytes)
         else:
-            h2d = int(P.corpus.packed_bytes(P.pack(mats)))
+            h2d = int(corpus_d.h2d_bytes)  # corpus upload (CSR + CSC + tables)
             d2h = int(res.scores.nbytes)
         e2e = {"value": n_units / statistics.mean(times), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "api": api}

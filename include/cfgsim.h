@@ -83,6 +83,10 @@ CFGSIM_API int cfgsim_device_count(int32_t *n);
 CFGSIM_API int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
                          const int64_t *rp_off, const int32_t *rowptr, const int64_t *nz_off,
                          const int32_t *col, const double *val, cfgsim_corpus **out);
+/* Same from dense row-major matrices (mats[g]: n_nodes[g]^2 doubles, the
+ * TransitionMatrix.entries themselves): the CSR is built natively. */
+CFGSIM_API int cfgsim_corpus_create_dense(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
+                                          const double *const *mats, cfgsim_corpus **out);
 CFGSIM_API int cfgsim_corpus_destroy(cfgsim_corpus *c);
 CFGSIM_API int cfgsim_corpus_info(const cfgsim_corpus *c, int32_t *n_graphs, int32_t *max_nodes,
                        int64_t *device_bytes);

@@ -46,6 +46,7 @@ _SIGS = {
     "cfgsim_version": ([], C.c_int),
     "cfgsim_device_count": ([_vp], C.c_int),
     "cfgsim_corpus_create": ([_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)], C.c_int),
+    "cfgsim_corpus_create_dense": ([_i32, _i32, _vp, _vp, C.POINTER(_vp)], C.c_int),
     "cfgsim_corpus_destroy": ([_vp], C.c_int),
     "cfgsim_corpus_info": ([_vp, _vp, _vp, _vp], C.c_int),
     "cfgsim_isorank_pairs": ([_vp, _vp, _i64, _vp, _vp, _pp, _vp, _vp, _vp, _vp, _vp], C.c_int),

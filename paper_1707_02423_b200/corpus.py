@@ -63,17 +63,30 @@ class DeviceCorpus:
     """A packed corpus resident in one GPU's HBM (``cfgsim_corpus_create``)."""
 
     def __init__(self, matrices_or_packed, device: int | None = None):
-        packed = matrices_or_packed if isinstance(matrices_or_packed, dict) else pack(matrices_or_packed)
         self.device = nat.default_device() if device is None else int(device)
-        self.n_nodes = packed["n_nodes"]
-        self.K = int(len(self.n_nodes))
-        self.h2d_bytes = packed_bytes(packed)
         h = nat.C.c_void_p()
-        nat.check(nat.lib.cfgsim_corpus_create(
-            self.device, self.K, nat.ptr(packed["n_nodes"]), nat.ptr(packed["rp_off"]),
-            nat.ptr(packed["rowptr"]), nat.ptr(packed["nz_off"]), nat.ptr(packed["col"]),
-            nat.ptr(packed["val"]), nat.C.byref(h)))
+        if isinstance(matrices_or_packed, dict):
+            packed = matrices_or_packed
+            self.n_nodes = packed["n_nodes"]
+            self.K = int(len(self.n_nodes))
+            nat.check(nat.lib.cfgsim_corpus_create(
+                self.device, self.K, nat.ptr(packed["n_nodes"]), nat.ptr(packed["rp_off"]),
+                nat.ptr(packed["rowptr"]), nat.ptr(packed["nz_off"]), nat.ptr(packed["col"]),
+                nat.ptr(packed["val"]), nat.C.byref(h)))
+        else:  # dense entries: the CSR is built natively (cfgsim_corpus_create_dense)
+            es = [np.ascontiguousarray(_entries(m)) for m in matrices_or_packed]
+            for g, e in enumerate(es):
+                if e.ndim != 2 or e.shape[0] != e.shape[1] or e.shape[0] < 1:
+                    raise ValueError(f"matrix {g}: entries must be square and non-empty, got {e.shape}")
+            self.n_nodes = np.array([e.shape[0] for e in es], np.int32)
+            self.K = len(es)
+            ptrs = (nat.C.c_void_p * self.K)(*[e.ctypes.data for e in es])
+            nat.check(nat.lib.cfgsim_corpus_create_dense(self.device, self.K, nat.ptr(self.n_nodes), ptrs,
+                                                         nat.C.byref(h)))
         self._h = h
+        info = np.zeros(1, np.int64)
+        nat.check(nat.lib.cfgsim_corpus_info(h, None, None, nat.ptr(info)))
+        self.h2d_bytes = int(info[0])
 
     @property
     def handle(self):

@@ -198,7 +198,7 @@ def pairwise(matrices: list[TransitionMatrix], measure: MeasureId, *, p: float =
     if measure is not MeasureId.ISO:
         # symmetric, zero diagonal, NaN where the measure fails (similarity.py:247-255)
         scores = np.empty((k, k))
-        with DeviceCorpus(pack(ordered), _dev(device)) as corpus:
+        with DeviceCorpus(ordered, _dev(device)) as corpus:
             nat.check(nat.lib.cfgsim_flat_allpairs(corpus.handle, nat.FLAT_IDS[measure.value], float(p),
                                                    nat.ptr(scores), None))
         pm = PairwiseMatrix(measure=measure, kernel_ids=ids, scores=scores, scaled=False)
@@ -207,7 +207,7 @@ def pairwise(matrices: list[TransitionMatrix], measure: MeasureId, *, p: float =
     scores = np.empty((k, k))
     iters = np.empty((k, k), np.int32) if return_iterations else None
     prm = nat.params(alpha, tol, max_iter, precision)
-    with DeviceCorpus(pack(ordered), _dev(device)) as corpus:
+    with DeviceCorpus(ordered, _dev(device)) as corpus:
         nat.check(nat.lib.cfgsim_allpairs(corpus.handle, 0 if symmetric else 1, nat.C.byref(prm),
                                           nat.ptr(scores), nat.ptr(iters), None))
     pm = PairwiseMatrix(measure=measure, kernel_ids=ids, scores=scores, scaled=False)
@@ -251,7 +251,7 @@ def nearest(queries: Sequence[TransitionMatrix], corpus: Sequence[TransitionMatr
     best_d = np.empty(nq)
     best_i = np.empty(nq, np.int64)
     prm = nat.params(alpha, tol, max_iter, precision)
-    with DeviceCorpus(pack(queries), dev) as Q, DeviceCorpus(pack(corpus), dev) as Cc:
+    with DeviceCorpus(queries, dev) as Q, DeviceCorpus(corpus, dev) as Cc:
         nat.check(nat.lib.cfgsim_nearest(Q.handle, Cc.handle, 0, Cc.K, nat.C.byref(prm), nat.ptr(best_d),
                                          nat.ptr(best_i), None))
     return best_d, best_i
