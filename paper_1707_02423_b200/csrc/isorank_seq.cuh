@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     };
     stage(0);
     int emn = 0x7fffffff, emx = -1;
-    if constexpr (sizeof(T) == 8) {
+    {
       // fp64 tensor cores: mma.m8n8k4 accumulates each 8x8 tile as the fma
       // chain over k in order (bitwise equal to the scalar chain, probed on
       // B200: tools/probes/dmma_probe.cu), so X is the same as the m-ascending
@@ -957,24 +957,24 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
           big_cp_async_wait_group<0>();
         }
         nbar_sync(BAR_P, NP);
-        const double *buf = (const double *)stg + (ch & 1) * P2_KC * SPD;
+        const T *buf = stg + (ch & 1) * P2_KC * SPD;  // (fp32 mode: rows promoted to fp64 for the mma)
         const int m0 = ch * P2_KC;
 #pragma unroll
         for (int k0 = 0; k0 < P2_KC; k0 += 4) {
           const int m = m0 + k0 + lk;  // this lane's k
           if (m0 + k0 > K) break;
           const double cf = (m < K) ? cfa[m] : (m == K ? cfk[m] : 0.0);
-          const double *row = buf + (k0 + lk) * SPD;
+          const T *row = buf + (k0 + lk) * SPD;
           double af[TR], bf[TC];
 #pragma unroll
           for (int x = 0; x < TR; x++) {
             const int i = (wr * TR + x) * 8 + lr;
-            af[x] = cf * (i < N ? row[i] : 0.0);
+            af[x] = cf * (i < N ? (double)row[i] : 0.0);
           }
 #pragma unroll
           for (int y = 0; y < TC; y++) {
             const int j = (wc * TC + y) * 8 + lr;
-            bf[y] = j < N ? row[NPt + j] : 0.0;
+            bf[y] = j < N ? (double)row[NPt + j] : 0.0;
           }
 #pragma unroll
           for (int x = 0; x < TR; x++)
@@ -1022,91 +1022,6 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
               else Xs[i * P + j] = (T)acc[x][y][h];
             }
           }
-    } else {
-      T Pacc[AR][BC];
-#pragma unroll
-      for (int x = 0; x < AR; x++)
-#pragma unroll
-        for (int y = 0; y < BC; y++) Pacc[x][y] = 0;
-      int ii[AR], jj[BC];
-#pragma unroll
-      for (int x = 0; x < AR; x++) { ii[x] = ty + TY * x; if (ii[x] >= N) ii[x] = N - 1; }
-#pragma unroll
-      for (int y = 0; y < BC; y++) { jj[y] = tx + TX * y; if (jj[y] >= N) jj[y] = N - 1; }
-      T uK[AR], vK[BC];
-      for (int ch = 0; ch < nch; ch++) {
-        if (ch + 1 < nch) {
-          stage(ch + 1);
-          big_cp_async_wait_group<1>();
-        } else {
-          big_cp_async_wait_group<0>();
-        }
-        nbar_sync(BAR_P, NP);
-        const T *buf = stg + (ch & 1) * P2_KC * SPD;
-        const int m0 = ch * P2_KC;
-        const int rows = (K + 1 - m0) < P2_KC ? (K + 1 - m0) : P2_KC;
-        if (owner) {
-          for (int mm = 0; mm < rows; mm++) {
-            const int m = m0 + mm;
-            const T *um = buf + mm * SPD, *vm = um + NPt;
-            if (m == K) {  // last term
-#pragma unroll
-              for (int x = 0; x < AR; x++) uK[x] = um[ii[x]];
-#pragma unroll
-              for (int y = 0; y < BC; y++) vK[y] = vm[jj[y]];
-              break;
-            }
-            const T cak = (T)cfa[m];
-            T vb[BC];
-#pragma unroll
-            for (int y = 0; y < BC; y++) vb[y] = vm[jj[y]];
-#pragma unroll
-            for (int x = 0; x < AR; x++) {
-              const T cu = cak * um[ii[x]];
-#pragma unroll
-              for (int y = 0; y < BC; y++) Pacc[x][y] = fma(cu, vb[y], Pacc[x][y]);
-            }
-          }
-        }
-        nbar_sync(BAR_P, NP);  // buffer (ch & 1) is re-staged by chunk ch + 2 / X overwrites it
-      }
-      if (owner) {
-        const T sc = (T)cfk[K];
-#pragma unroll
-        for (int x = 0; x < AR; x++) {
-          const T su = sc * uK[x];
-#pragma unroll
-          for (int y = 0; y < BC; y++) {
-            Pacc[x][y] = fma(su, vK[y], Pacc[x][y]);
-            if (ty + TY * x < N && tx + TX * y < N) {
-              const int e = big_exponent(Pacc[x][y]);
-              emn = min(emn, e);
-              emx = max(emx, e);
-            }
-          }
-        }
-        emn = __reduce_min_sync(__activemask(), emn);
-        emx = __reduce_max_sync(__activemask(), emx);
-        if (lane == 0 || !(__activemask() & ((1u << lane) - 1))) {
-          atomicMin(s_first + 1, emn);
-          atomicMax(s_first + 2, emx);
-        }
-      }
-      nbar_sync(BAR_P, NP);
-      const int emin = s_first[1];
-      constexpr int PK = 32 * KB + 1;
-      unsigned long long *Kr = (unsigned long long *)Xs;
-      if (owner) {
-#pragma unroll
-        for (int x = 0; x < AR; x++) {
-          const int i = ty + TY * x;
-#pragma unroll
-          for (int y = 0; y < BC; y++) {
-            const int j = tx + TX * y;
-            if (i < N && j < N) Kr[i * PK + j] = p2_key<T>(Pacc[x][y], j, emin);
-          }
-        }
-      }
     }
     nbar_sync(BAR_P, NP);
     const int emin = s_first[1];

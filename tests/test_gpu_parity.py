@@ -303,7 +303,7 @@ def test_lowrank_and_two_product_kernels_agree(P):
 def test_two_stage_matches_per_pair_kernel(P):
     """Two-stage all-pairs (per-(graph, N) sequences, then per-pair rank-K
     products; isorank_seq.cuh) against the per-pair low-rank kernel
-    (CFGSIM_TWOSTAGE=0): identical iteration counts, bitwise-equal d."""
+    (CFGSIM_TWOSTAGE=0): identical iteration counts, bitwise-equal d in fp64."""
     import os
     import subprocess
     import sys
@@ -324,7 +324,10 @@ def test_two_stage_matches_per_pair_kernel(P):
             outs.append(np.load(path))
         n = len(outs[0]) // 2
         np.testing.assert_array_equal(outs[0][n:], outs[1][n:])
-        np.testing.assert_array_equal(outs[0][:n], outs[1][:n])
+        if prec == "fp64":  # same fma chain (fp64 mma == sequential fma): bitwise
+            np.testing.assert_array_equal(outs[0][:n], outs[1][:n])
+        else:  # fp32 mode forms the rank-K product in fp64 on the tensor cores
+            np.testing.assert_allclose(outs[0][:n], outs[1][:n], rtol=1e-6)
 
 
 def test_nearest_mixed_sizes_matches_oracle(P):
