@@ -163,6 +163,14 @@ CFGSIM_API int cfgsim_flat_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B,
 CFGSIM_API int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, double p, double *d_mat,
                                     void *cuda_stream);
 
+/* export_heatmap_csv (similarity.py:287-293), native and multi-threaded (host
+ * code; the K x K text for K = 20k is ~4 GB): ids = concatenated UTF-8
+ * kernel ids, id_off[k+1] their byte offsets, scores K x K row-major.  With
+ * out == NULL only *len (bytes) is returned; else out needs cap >= *len.
+ * Byte-identical to the reference's f"{x:.6f}" / "nan" formatting. */
+CFGSIM_API int cfgsim_heatmap_csv(int32_t k, const char *ids, const int64_t *id_off, const double *scores,
+                                  char *out, int64_t cap, int64_t *len, int32_t threads);
+
 /* Number of pair-kernel launches issued by this process so far (bench
  * evidence for gpu_launches). */
 CFGSIM_API int64_t cfgsim_launch_count(void);

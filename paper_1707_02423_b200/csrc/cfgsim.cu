@@ -17,6 +17,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cfgsim.h"
@@ -1758,6 +1759,58 @@ int cfgsim_flat_single(int32_t device, int32_t na, const double *A, int32_t nb, 
   if (std::isnan(*out)) return fail(CFGSIM_ERR_DEGENERATE, measure == CFGSIM_JAC
                                                              ? "jaccard undefined for two all-zero matrices"
                                                              : "cosine undefined for an all-zero matrix");
+  return CFGSIM_OK;
+}
+
+int cfgsim_heatmap_csv(int32_t k, const char *ids, const int64_t *id_off, const double *scores, char *out,
+                       int64_t cap, int64_t *len, int32_t threads) {
+  // export_heatmap_csv (similarity.py:287-293): header ",id0,id1,...", then
+  // per row "id," + cells joined by ",", each "%.6f" or "nan" when not finite;
+  // "\n" after every line.  Rows are formatted in parallel, then concatenated.
+  if (k < 0 || (k && (!ids || !id_off || !scores)) || !len) return fail(CFGSIM_ERR_ARG, "bad csv arguments");
+  const int nt = std::max(1, std::min<int>(threads > 0 ? threads : (int)std::thread::hardware_concurrency(), 256));
+  std::vector<std::string> rows(k);
+  auto work = [&](int t) {
+    char buf[64];
+    for (int64_t r = t; r < k; r += nt) {
+      std::string &s = rows[r];
+      s.reserve((size_t)k * 9 + 32);
+      s.append(ids + id_off[r], ids + id_off[r + 1]);
+      for (int64_t q = 0; q < k; q++) {
+        const double x = scores[r * (int64_t)k + q];
+        s.push_back(',');
+        if (!std::isfinite(x)) {
+          s.append("nan");
+        } else {
+          const int m = snprintf(buf, sizeof(buf), "%.6f", x);
+          s.append(buf, (size_t)m);
+        }
+      }
+      s.push_back('\n');
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto &th : pool) th.join();
+  std::string head = ",";
+  for (int64_t r = 0; r < k; r++) {
+    if (r) head.push_back(',');
+    head.append(ids + id_off[r], ids + id_off[r + 1]);
+  }
+  head.push_back('\n');
+  int64_t total = (int64_t)head.size();
+  for (auto &s : rows) total += (int64_t)s.size();
+  *len = total;
+  if (!out) return CFGSIM_OK;  // size query
+  if (cap < total) return fail(CFGSIM_ERR_ARG, "csv buffer too small");
+  char *p = out;
+  memcpy(p, head.data(), head.size());
+  p += head.size();
+  for (auto &s : rows) {
+    memcpy(p, s.data(), s.size());
+    p += s.size();
+  }
   return CFGSIM_OK;
 }
 

@@ -230,8 +230,25 @@ def minmax_scale(pm: PairwiseMatrix) -> PairwiseMatrix:
     return PairwiseMatrix(measure=pm.measure, kernel_ids=pm.kernel_ids, scores=out, scaled=True)
 
 
-def export_heatmap_csv(pm: PairwiseMatrix) -> str:
-    """CSV, kernel_id header row/column, 6 decimals, ``nan`` (``similarity.py:287-293``)."""
+def export_heatmap_csv(pm: PairwiseMatrix, *, native: bool | None = None) -> str:
+    """CSV, kernel_id header row/column, 6 decimals, ``nan`` (``similarity.py:287-293``).
+
+    Large matrices (K >= 64, or native=True) are formatted by the library's
+    multi-threaded writer (``cfgsim_heatmap_csv``), byte-identical to the
+    Python formatting below."""
+    k = len(pm.kernel_ids)
+    if native or (native is None and k >= 64):
+        enc = [kid.encode() for kid in pm.kernel_ids]
+        ids = np.frombuffer(b"".join(enc), np.uint8) if enc else np.zeros(0, np.uint8)
+        off = np.zeros(k + 1, np.int64)
+        off[1:] = np.cumsum([len(e) for e in enc])
+        sc = np.ascontiguousarray(pm.scores, dtype=np.float64)
+        n = np.zeros(1, np.int64)
+        nat.check(nat.lib.cfgsim_heatmap_csv(k, nat.ptr(ids), nat.ptr(off), nat.ptr(sc), None, 0, nat.ptr(n), 0))
+        buf = np.empty(int(n[0]), np.uint8)
+        nat.check(nat.lib.cfgsim_heatmap_csv(k, nat.ptr(ids), nat.ptr(off), nat.ptr(sc), nat.ptr(buf), int(n[0]),
+                                             nat.ptr(n), 0))
+        return buf.tobytes().decode()
     header = "," + ",".join(pm.kernel_ids)
     body = [
         kid + "," + ",".join(f"{v:.6f}" if np.isfinite(v) else "nan" for v in row)

@@ -97,3 +97,23 @@ def test_minmax_and_csv_match_reference_semantics():
                                                      "k1.s.t.h,nan,0.000000"]
     with pytest.raises(P.DegenerateInput):
         P.minmax_scale(P.PairwiseMatrix(P.MeasureId.EUC, ids, np.array([[0.0, np.nan], [np.nan, 0.0]])))
+
+
+def test_native_csv_writer_byte_identical():
+    """cfgsim_heatmap_csv (host code, runs without a GPU) against the
+    reference's formatting (similarity.py:287-293) and its golden bytes."""
+    import paper_1707_02423_b200 as P
+    from conftest import GOLDEN, load_golden
+    rng = np.random.default_rng(12)
+    for k in (1, 2, 65, 300):
+        sc = rng.random((k, k)) * 2.0
+        sc[rng.random((k, k)) < 0.02] = np.nan
+        if k > 1:
+            sc[0, 1], sc[1, 0] = np.inf, -0.0
+        sc[0, 0] = 0.0000005  # half-way cases round on the exact binary value
+        ids = tuple(f"k{i:04d}.k.x.y" for i in range(k))
+        pm = P.PairwiseMatrix(P.MeasureId.ISO, ids, sc)
+        assert P.export_heatmap_csv(pm, native=True) == P.export_heatmap_csv(pm, native=False)
+    g = load_golden("bundled_corpus.npz")
+    pm = P.PairwiseMatrix(P.MeasureId.ISO, tuple(str(x) for x in g["ids"]), g["scores"])
+    assert P.export_heatmap_csv(pm, native=True) == (GOLDEN / "iso.csv").read_text()
