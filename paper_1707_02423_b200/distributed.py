@@ -150,3 +150,94 @@ def nearest_sharded(n_corpus: int, compute_shard: Callable[[int, int], tuple], *
     dist.all_gather_into_tensor(gi, ti, group=group)
     best, idx = merge_best(gd.view(world, -1), gi.view(world, -1))
     return best.cpu().numpy(), idx.cpu().numpy()
+
+
+def _world(group):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def pairwise_sharded(matrices, *, alpha: float = 0.85, tol: float = 1e-9, max_iter: int = 1000,
+                     precision: str = "fp64", device: int | None = None, group=None):
+    """``pairwise(matrices, MeasureId.ISO)`` across the ranks of a
+    torch.distributed group (one GPU per rank): each rank uploads the corpus,
+    aligns its cost-balanced share of the size-sorted upper triangle, one
+    all-gather (NCCL over NVLink) assembles the unit vector, the K x K matrix
+    is scattered on the device and returned on every rank.  Same result as
+    ``pairwise`` bitwise, for any world size."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _native as nat
+    from .corpus import DeviceCorpus
+    from .errors import DuplicateKernel
+    from .similarity import MeasureId, PairwiseMatrix, _check_alpha
+
+    if len(matrices) < 2:
+        raise ValueError("pairwise comparison needs at least 2 kernels")
+    ordered = sorted(matrices, key=lambda m: m.kernel_id)
+    ids = tuple(m.kernel_id for m in ordered)
+    if len(set(ids)) != len(ids):
+        raise DuplicateKernel("duplicate kernel_id in pairwise input")
+    _check_alpha(alpha)
+    world, rank = _world(group)
+    dev_idx = nat.default_device() if device is None else int(device)
+    dev = torch.device("cuda", dev_idx)
+    prm = nat.params(alpha, tol, max_iter, precision)
+    k = len(ordered)
+    with DeviceCorpus(ordered, dev_idx) as C:
+        bounds = C.split(world)
+        u0, u1 = int(bounds[rank]), int(bounds[rank + 1])
+        chunk = max(int(max(bounds[1:] - bounds[:-1])), 1)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        d_lin = torch.zeros(chunk, dtype=torch.float64, device=dev)
+        if u1 > u0:
+            nat.check(nat.lib.cfgsim_allpairs_range(C.handle, u0, u1, 0, nat.C.byref(prm), nat.ptr(d_lin), None, st))
+        if world > 1:
+            gathered = torch.empty(world * chunk, dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(gathered, d_lin, group=group)
+            full = torch.cat([gathered[r * chunk:r * chunk + int(bounds[r + 1] - bounds[r])] for r in range(world)])
+        else:
+            full = d_lin[: u1 - u0]
+        scores_d = torch.empty((k, k), dtype=torch.float64, device=dev)
+        nat.check(nat.lib.cfgsim_allpairs_scatter(C.handle, 0, nat.ptr(full), None, nat.ptr(scores_d), None, st))
+        scores = scores_d.cpu().numpy()
+    return PairwiseMatrix(measure=MeasureId.ISO, kernel_ids=ids, scores=scores, scaled=False)
+
+
+def nearest_gpu_sharded(queries, corpus, *, alpha: float = 0.85, tol: float = 1e-9, max_iter: int = 1000,
+                        precision: str = "fp64", device: int | None = None, group=None):
+    """``nearest(queries, corpus)`` across the ranks of a torch.distributed
+    group: rank r searches corpus shard r (``cfgsim_nearest`` on [c0, c1)),
+    one all-gather of the (d, index) candidates, lexicographic minimum."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _native as nat
+    from .corpus import DeviceCorpus
+    from .similarity import _check_alpha
+
+    _check_alpha(alpha)
+    world, rank = _world(group)
+    dev_idx = nat.default_device() if device is None else int(device)
+    dev = torch.device("cuda", dev_idx)
+    prm = nat.params(alpha, tol, max_iter, precision)
+    nq, nc = len(queries), len(corpus)
+    bounds = np.linspace(0, nc, world + 1).astype(np.int64)
+    c0, c1 = int(bounds[rank]), int(bounds[rank + 1])
+    bd = torch.full((nq,), float("inf"), dtype=torch.float64, device=dev)
+    bi = torch.full((nq,), np.iinfo(np.int64).max, dtype=torch.int64, device=dev)
+    with DeviceCorpus(queries, dev_idx) as Q, DeviceCorpus(corpus, dev_idx) as Cc:
+        st = torch.cuda.current_stream(dev).cuda_stream
+        if c1 > c0:
+            nat.check(nat.lib.cfgsim_nearest(Q.handle, Cc.handle, c0, c1, nat.C.byref(prm), nat.ptr(bd), nat.ptr(bi),
+                                             st))
+        if world > 1:
+            gd = torch.empty(world * nq, dtype=torch.float64, device=dev)
+            gi = torch.empty(world * nq, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(gd, bd, group=group)
+            dist.all_gather_into_tensor(gi, bi, group=group)
+            bd, bi = merge_best(gd.view(world, nq), gi.view(world, nq))
+        return bd.cpu().numpy(), bi.cpu().numpy()

@@ -355,3 +355,19 @@ def test_nearest_mixed_sizes_matches_oracle(P):
         dl, *_ = P.isorank_pairs(CQ, CC, np.repeat(np.arange(len(q)), len(c)), np.tile(np.arange(len(c)), len(q)))
     bd, bi = P.nearest(q, c)
     np.testing.assert_array_equal(bd, dl.reshape(len(q), len(c)).min(axis=1))
+
+
+def test_sharded_api_single_rank_matches(P):
+    """distributed.pairwise_sharded / nearest_gpu_sharded (world 1) equal the
+    unsharded API bitwise."""
+    from paper_1707_02423_b200 import distributed as D
+    from paper_1707_02423_b200 import synth
+    mats = synth.random_corpus(40, 8, 150, seed=77)
+    tms = [P.TransitionMatrix(f"g{i:03d}.s.h.d", m, tuple(range(len(m))), P.ROW_STOCHASTIC) for i, m in enumerate(mats)]
+    a = P.pairwise(tms, P.MeasureId.ISO).scores
+    b = D.pairwise_sharded(tms[::-1]).scores
+    np.testing.assert_array_equal(a, b)
+    bd, bi = P.nearest(mats[:5], mats[5:])
+    sd, si = D.nearest_gpu_sharded(mats[:5], mats[5:])
+    np.testing.assert_array_equal(bd, sd)
+    np.testing.assert_array_equal(bi, si)
