@@ -371,3 +371,22 @@ def test_sharded_api_single_rank_matches(P):
     sd, si = D.nearest_gpu_sharded(mats[:5], mats[5:])
     np.testing.assert_array_equal(bd, sd)
     np.testing.assert_array_equal(bi, si)
+
+
+@pytest.mark.parametrize("alpha,tol,max_iter", [(0.85, 1e-9, 1), (0.85, 1e-9, 3), (0.85, 1e-9, 7), (0.5, 1e-12, 1000),
+                                                (0.95, 1e-9, 1000), (0.99, 1e-9, 1000), (0.85, 1e-6, 50)])
+def test_allpairs_parameters_match_oracle(P, alpha, tol, max_iter):
+    """Parameter corners through the all-pairs path (two-stage for kcap <= 512,
+    the per-pair low-rank kernel beyond, e.g. alpha = 0.99): iteration cut-offs,
+    convergence flags, d against the oracle."""
+    from oracle import ffi
+    from paper_1707_02423_b200 import synth
+    mats = synth.random_corpus(24, 4, 64, seed=int(alpha * 100) + max_iter)
+    k = len(mats)
+    tms = [P.TransitionMatrix(f"g{i:03d}.p.c.t", m, tuple(range(len(m))), P.ROW_STOCHASTIC) for i, m in enumerate(mats)]
+    pm, iters = P.pairwise(tms, P.MeasureId.ISO, alpha=alpha, tol=tol, max_iter=max_iter, return_iterations=True)
+    iu, ju = np.triu_indices(k)
+    d, w, it, cv = ffi.iso_batch(P.pack(mats), iu.astype(np.int32), ju.astype(np.int32), alpha=alpha, tol=tol,
+                                 max_iter=max_iter)
+    np.testing.assert_array_equal(iters[iu, ju], it)
+    np.testing.assert_allclose(pm.scores[iu, ju], d, rtol=RTOL64)
