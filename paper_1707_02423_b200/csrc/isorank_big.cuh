@@ -281,11 +281,6 @@ __device__ __forceinline__ int big_key_col(unsigned long long k) {
   return (1 << BIG_CB) - 1 - (int)(k & ((1ull << BIG_CB) - 1));
 }
 
-__device__ __forceinline__ void big_cp_async8(void *smem_dst, const void *gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
-
 __device__ __forceinline__ void big_cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // B-byte async copy global -> shared; zero-fills the destination when !valid

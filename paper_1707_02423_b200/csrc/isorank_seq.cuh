@@ -16,11 +16,12 @@
 //  stage 2 (isorank_pair2_kernel): per pair, the stopping sweep K from the
 //    bracket  (alpha^k/N) max(Du_k, Dv_k) <= delta_k <= (alpha^k/N)(Du_k + Dv_k)
 //    (exact delta_k, an N^2 pass, only where the bracket straddles tol),
-//    then X_K as a rank-K product accumulated in registers in the low-rank
-//    kernel's order (m ascending), the greedy matching and d.
+//    then X_K as a rank-K product on the fp64 tensor cores (mma.m8n8k4: the
+//    low-rank kernel's m-ascending fma chain, bitwise), the row orders, the
+//    greedy matching (a consumer warp overlapping the next pair) and d.
 //
 // Per pair this removes every sweep barrier and mat-vec: what remains is
-// ~K N^2 FMAs, one sort per row and N greedy rounds.
+// ~K N^2 mma work, one sort per row and N greedy rounds.
 #pragma once
 #include "isorank_lr.cuh"
 #include "isorank_big.cuh"
@@ -520,36 +521,6 @@ __device__ __forceinline__ double p2_key_value(unsigned long long k, int emin) {
   return (double)__uint_as_float((unsigned)(k >> 6));
 }
 
-__device__ __forceinline__ void p2_cx(unsigned long long &a, unsigned long long &b, bool desc) {
-  const bool sw = desc ? (b > a) : (a > b);
-  const unsigned long long x = sw ? b : a, y = sw ? a : b;
-  a = x;
-  b = y;
-}
-
-// Bitonic sort of 32 keys held by one thread (static register indices).
-__device__ __forceinline__ void p2_sort32(unsigned long long (&v)[32], bool desc) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-      for (int i = 0; i < 32; i++) {
-        const int l = i ^ j;
-        if (l > i) p2_cx(v[i], v[l], ((i & k) == 0) == desc);
-      }
-}
-// Bitonic merge of a bitonic 32-sequence held by one thread.
-__device__ __forceinline__ void p2_merge32(unsigned long long (&v)[32], bool desc) {
-#pragma unroll
-  for (int j = 16; j > 0; j >>= 1)
-#pragma unroll
-    for (int i = 0; i < 32; i++) {
-      const int l = i ^ j;
-      if (l > i) p2_cx(v[i], v[l], desc);
-    }
-}
-
 // Bitonic sort (descending) of n = 32 KB 32-bit keys held by one thread.
 template <int KB>
 __device__ __forceinline__ void p2_sort_u32(uint32_t (&v)[32 * KB]) {
@@ -787,9 +758,6 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   }
 
   // ---------------- producers
-  const int TY = prm.ty, TX = prm.tx;
-  const bool owner = tid < TY * TX;
-  const int ty = owner ? tid / TX : 0, tx = owner ? tid - (tid / TX) * TX : 0;
   const double invN = 1.0 / (double)N;
   const double c = (1.0 - prm.alpha) * inv_nn;
   const int mmax = prm.max_iter < prm.kcap ? prm.max_iter : prm.kcap;
