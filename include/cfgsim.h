@@ -171,6 +171,12 @@ CFGSIM_API int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, dou
 CFGSIM_API int cfgsim_heatmap_csv(int32_t k, const char *ids, const int64_t *id_off, const double *scores,
                                   char *out, int64_t cap, int64_t *len, int32_t threads);
 
+/* ward_linkage (cluster.py:88-134) on the GPU, exact (same double arithmetic
+ * and tie rule, O(k^2) work): features k x dim row-major [host]; k-1 merges
+ * out (ids a < b, leaves 0..k-1, merged k..2k-2; distance; merged size). */
+CFGSIM_API int cfgsim_ward(int32_t device, int32_t k, int32_t dim, const double *features, int64_t *out_a,
+                           int64_t *out_b, double *out_d, int64_t *out_size);
+
 /* Number of pair-kernel launches issued by this process so far (bench
  * evidence for gpu_launches). */
 CFGSIM_API int64_t cfgsim_launch_count(void);

@@ -63,6 +63,7 @@ _SIGS = {
     "cfgsim_flat_pairs": ([_vp, _vp, _i64, _vp, _vp, _i32, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_flat_allpairs": ([_vp, _i32, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_heatmap_csv": ([_i32, _vp, _vp, _vp, _vp, _i64, _vp, _i32], C.c_int),
+    "cfgsim_ward": ([_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "cfgsim_launch_count": ([], C.c_int64),
 }
 for _name, (_args, _res) in _SIGS.items():

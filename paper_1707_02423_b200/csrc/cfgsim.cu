@@ -25,6 +25,7 @@
 #include "tiers.h"
 #include "isorank_lr.cuh"
 #include "flat.cuh"
+#include "ward.cuh"
 
 using namespace cfgsim;
 
@@ -1811,6 +1812,80 @@ int cfgsim_heatmap_csv(int32_t k, const char *ids, const int64_t *id_off, const 
     memcpy(p, s.data(), s.size());
     p += s.size();
   }
+  return CFGSIM_OK;
+}
+
+int cfgsim_ward(int32_t device, int32_t k, int32_t dim, const double *features, int64_t *out_a, int64_t *out_b,
+                double *out_d, int64_t *out_size) {
+  // ward_linkage (cluster.py:88-134) on the GPU: k feature vectors of length
+  // dim (row-major host array); k - 1 merges (a < b ids, distance, size).
+  if (k < 2 || dim < 0 || (dim && !features) || !out_a || !out_b || !out_d || !out_size)
+    return fail(CFGSIM_ERR_ARG, "clustering needs at least 2 vectors");
+  if (int rc = set_device(device)) return rc;
+  DBuf D, id, sz, rmin, rarg, alive, flag, oa, ob, od, os;
+  CU(D.alloc(sizeof(double) * (size_t)k * k));
+  CU(id.alloc(sizeof(int64_t) * k));
+  CU(sz.alloc(sizeof(int64_t) * k));
+  CU(rmin.alloc(sizeof(double) * k));
+  CU(rarg.alloc(sizeof(int32_t) * k));
+  CU(alive.alloc(k));
+  CU(flag.alloc(sizeof(int32_t) * k));
+  CU(oa.alloc(sizeof(int64_t) * k));
+  CU(ob.alloc(sizeof(int64_t) * k));
+  CU(od.alloc(sizeof(double) * k));
+  CU(os.alloc(sizeof(int64_t) * k));
+  // Initial squared distances exactly as cluster.py:109-113 evaluates them:
+  // sum((x - y) ** 2 for ...) — libm pow(d, 2.0) (float ** 2 in CPython; not
+  // always the rounded product) summed by Python's sum(): 0 + first term, then
+  // Neumaier-compensated addition (CPython >= 3.12).  Host threads; the
+  // O(K^2 dim) pass is small next to the merge loop's K^2 updates.
+  {
+    std::vector<double> Dh((size_t)k * k, 0.0);
+    const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 64));
+    auto work = [&](int t) {
+      for (int64_t i = t; i < k; i += nt)
+        for (int64_t j = i + 1; j < k; j++) {
+          const double *x = features + i * dim, *y = features + j * dim;
+          double f = 0.0, cmp = 0.0;
+          for (int q = 0; q < dim; q++) {
+            const double v = std::pow(x[q] - y[q], 2.0);
+            if (q == 0) { f = v; continue; }  // int 0 + float: exact
+            const double tt = f + v;
+            if (std::fabs(f) >= std::fabs(v)) cmp += (f - tt) + v;
+            else cmp += (v - tt) + f;
+            f = tt;
+          }
+          if (cmp != 0.0 && std::isfinite(cmp)) f += cmp;
+          Dh[(size_t)i * k + j] = f;
+          Dh[(size_t)j * k + i] = f;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; t++) pool.emplace_back(work, t);
+    work(0);
+    for (auto &th : pool) th.join();
+    CU(cudaMemcpy(D.p, Dh.data(), sizeof(double) * (size_t)k * k, cudaMemcpyHostToDevice));
+  }
+  WardState ws;
+  ws.K = k;
+  ws.D = D.as<double>();
+  ws.id = id.as<int64_t>();
+  ws.size = sz.as<int64_t>();
+  ws.rmin = rmin.as<double>();
+  ws.rarg = rarg.as<int32_t>();
+  ws.alive = alive.as<uint8_t>();
+  ws.flag = flag.as<int32_t>();
+  ws.out_a = oa.as<int64_t>();
+  ws.out_b = ob.as<int64_t>();
+  ws.out_size = os.as<int64_t>();
+  ws.out_d = od.as<double>();
+  ward_kernel<<<1, WARD_THREADS>>>(ws);
+  g_launches += 2;
+  CU(cudaGetLastError());
+  CU(cudaMemcpy(out_a, oa.p, sizeof(int64_t) * (k - 1), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(out_b, ob.p, sizeof(int64_t) * (k - 1), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(out_d, od.p, sizeof(double) * (k - 1), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(out_size, os.p, sizeof(int64_t) * (k - 1), cudaMemcpyDeviceToHost));
   return CFGSIM_OK;
 }
 
