@@ -34,6 +34,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 from pathlib import Path
 
@@ -179,8 +180,21 @@ class Clocks:
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, FileNotFoundError):
             self.proc = None
+        self.first = ""
+        if self.proc is not None:
+            # nvidia-smi's start-up holds the driver for a while on a fresh box and would stall the
+            # first timed step's launches: wait for its first sample before timing starts
+            t = threading.Thread(target=self._first_line, daemon=True)
+            t.start()
+            t.join(timeout=10.0)
         time.sleep(0.3)
         return self
+
+    def _first_line(self):
+        try:
+            self.first = self.proc.stdout.readline()
+        except (OSError, ValueError):
+            pass
 
     def __exit__(self, *exc):
         self.out = ""
@@ -188,6 +202,7 @@ class Clocks:
             self.proc.terminate()
             try:
                 self.out, _ = self.proc.communicate(timeout=5)
+                self.out = self.out or self.first  # samples from the timed region; the idle one only as a fallback
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 self.out = ""

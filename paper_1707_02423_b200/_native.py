@@ -17,6 +17,8 @@ import numpy as np
 from .errors import BadOrder, DegenerateInput, DeviceError, DimMismatch
 
 LIB_PATH = Path(__file__).resolve().parent / "libcfgsim.so"
+if os.environ.get("CFGSIM_LIBRARY"):  # A/B runs of alternative builds of the same library
+    LIB_PATH = Path(os.environ["CFGSIM_LIBRARY"]).resolve()
 
 OK, ERR_ARG, ERR_DIM, ERR_CUDA, ERR_NOMEM, ERR_NODEVICE, ERR_DEGENERATE, ERR_ORDER = range(8)
 FLAT_IDS = {"euc": 0, "man": 1, "min": 2, "jac": 3, "cos": 4}
