@@ -47,6 +47,20 @@ extern "C" {
 #define CFGSIM_ERR_NODEVICE 5 /* no usable sm_100 device: there is no CPU path  */
 #define CFGSIM_ERR_DEGENERATE 6 /* measure undefined (reference: DegenerateInput) */
 #define CFGSIM_ERR_ORDER 7    /* Minkowski order p < 1 (reference: BadOrder)    */
+/* loader errors (errors.py:10-65) */
+#define CFGSIM_ERR_LISTING_SYNTAX 8   /* ListingSyntaxError(line_no, reason)     */
+#define CFGSIM_ERR_UNRESOLVED_LABEL 9 /* UnresolvedLabel                         */
+#define CFGSIM_ERR_PROFILE_SYNTAX 10  /* ProfileSyntaxError(line_no, reason)     */
+#define CFGSIM_ERR_DUPLICATE_KERNEL 11 /* DuplicateKernel                        */
+#define CFGSIM_ERR_EMPTY_GRAPH 12     /* EmptyGraph                              */
+#define CFGSIM_ERR_CORPUS 13          /* CorpusError (no profile for the kernel) */
+#define CFGSIM_ERR_VALUE 14           /* ValueError from KernelProfile checks    */
+#define CFGSIM_ERR_INDEX 15           /* IndexError (time_ns / calls without a value) */
+
+/* transition-matrix modes (matrix.py:17-19) */
+#define CFGSIM_MODE_ROW_STOCHASTIC 0
+#define CFGSIM_MODE_GLOBAL 1
+#define CFGSIM_MODE_RAW_COUNTS 2
 
 /* flat measures (similarity.py:20-66) */
 #define CFGSIM_EUC 0
@@ -176,6 +190,30 @@ CFGSIM_API int cfgsim_heatmap_csv(int32_t k, const char *ids, const int64_t *id_
  * out (ids a < b, leaves 0..k-1, merged k..2k-2; distance; merged size). */
 CFGSIM_API int cfgsim_ward(int32_t device, int32_t k, int32_t dim, const double *features, int64_t *out_a,
                            int64_t *out_b, double *out_d, int64_t *out_size);
+
+/* Corpus loader, host code, multi-threaded over kernels:
+ * listing text (+ optional profile text) per kernel -> transition matrix in
+ * canonical order.  Replaces, per kernel, cli.py:55-74 _load_kernel
+ * (parse_listing sass.py:162-221, build_cfg cfg.py:186-259, parse_profiles
+ * profile.py:74-151, attribute_profile profile.py:178-233) followed by
+ * transition_matrix (matrix.py:45-71), with identical entries and ordering.
+ * profiles may be NULL, or hold NULL for kernels without a profile.  All
+ * kernels are processed; the return value is the first failing kernel's code
+ * (input order) and cfgsim_matrices_status() has every kernel's code, line
+ * number and the reference's message.  *out is set whenever the return is not
+ * CFGSIM_ERR_ARG / CFGSIM_ERR_NOMEM; free it with cfgsim_matrices_destroy. */
+typedef struct cfgsim_matrices cfgsim_matrices;
+CFGSIM_API int cfgsim_matrices_from_listings(int32_t count, const char *const *kernel_ids,
+                                             const char *const *listings, const int64_t *listing_lens,
+                                             const char *const *profiles, const int64_t *profile_lens,
+                                             int32_t mode, int32_t n_threads, cfgsim_matrices **out);
+/* sizes[count] (0 for failed kernels) and the total number of entries */
+CFGSIM_API int cfgsim_matrices_sizes(const cfgsim_matrices *m, int32_t *sizes, int64_t *total_entries);
+/* concatenated row-major entries (sum n^2) and canonical orderings (sum n) */
+CFGSIM_API int cfgsim_matrices_read(const cfgsim_matrices *m, double *entries, int32_t *orderings);
+CFGSIM_API int cfgsim_matrices_status(const cfgsim_matrices *m, int32_t index, int32_t *code, int64_t *line_no,
+                                      char *msg, int64_t cap);
+CFGSIM_API void cfgsim_matrices_destroy(cfgsim_matrices *m);
 
 /* Number of pair-kernel launches issued by this process so far (bench
  * evidence for gpu_launches). */

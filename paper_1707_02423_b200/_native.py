@@ -21,6 +21,9 @@ if os.environ.get("CFGSIM_LIBRARY"):  # A/B runs of alternative builds of the sa
     LIB_PATH = Path(os.environ["CFGSIM_LIBRARY"]).resolve()
 
 OK, ERR_ARG, ERR_DIM, ERR_CUDA, ERR_NOMEM, ERR_NODEVICE, ERR_DEGENERATE, ERR_ORDER = range(8)
+(ERR_LISTING_SYNTAX, ERR_UNRESOLVED_LABEL, ERR_PROFILE_SYNTAX, ERR_DUPLICATE_KERNEL, ERR_EMPTY_GRAPH, ERR_CORPUS,
+ ERR_VALUE, ERR_INDEX) = range(8, 16)
+MODE_IDS = {"row_stochastic": 0, "global": 1, "raw_counts": 2}
 FLAT_IDS = {"euc": 0, "man": 1, "min": 2, "jac": 3, "cos": 4}
 FP64, FP32 = 0, 1
 
@@ -66,6 +69,11 @@ _SIGS = {
     "cfgsim_flat_allpairs": ([_vp, _i32, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_heatmap_csv": ([_i32, _vp, _vp, _vp, _vp, _i64, _vp, _i32], C.c_int),
     "cfgsim_ward": ([_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "cfgsim_matrices_from_listings": ([_i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.POINTER(_vp)], C.c_int),
+    "cfgsim_matrices_sizes": ([_vp, _vp, _vp], C.c_int),
+    "cfgsim_matrices_read": ([_vp, _vp, _vp], C.c_int),
+    "cfgsim_matrices_status": ([_vp, _i32, _vp, _vp, C.c_char_p, _i64], C.c_int),
+    "cfgsim_matrices_destroy": ([_vp], None),
     "cfgsim_launch_count": ([], C.c_int64),
 }
 for _name, (_args, _res) in _SIGS.items():
