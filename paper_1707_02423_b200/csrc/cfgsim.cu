@@ -1106,30 +1106,68 @@ int check_flat(int32_t measure, double p) {
 }  // namespace
 
 // ====================================================================== C ABI
-extern "C" {
-
-const char *cfgsim_last_error(void) { return g_err.c_str(); }
-int cfgsim_version(void) { return 100; }
-int64_t cfgsim_launch_count(void) { return g_launches.load(); }
-
-int cfgsim_device_count(int32_t *n) {
-  if (!n) return fail(CFGSIM_ERR_ARG, "n is NULL");
-  *n = 0;
-  int c = 0;
-  if (cudaGetDeviceCount(&c) != cudaSuccess) {
-    cudaGetLastError();
-    return CFGSIM_OK;
+namespace {
+// run f(g) for g in [0, n) on the host cores (graph-parallel packing)
+template <typename F>
+void parallel_graphs(int n, F f) {
+  static const int cap = [] {  // CFGSIM_HOST_THREADS: host packing threads (default: all cores, <= 32)
+    const char *e = getenv("CFGSIM_HOST_THREADS");
+    return e && atoi(e) > 0 ? atoi(e) : std::min(32, (int)std::thread::hardware_concurrency());
+  }();
+  const int nt = std::max(1, std::min<int>(cap, n / 64 + 1));
+  if (nt == 1) {
+    for (int g = 0; g < n; g++) f(g);
+    return;
   }
-  for (int i = 0; i < c; i++) {
-    cudaDeviceProp pr;
-    if (cudaGetDeviceProperties(&pr, i) == cudaSuccess && pr.major == 10) (*n)++;
-  }
-  return CFGSIM_OK;
+  std::atomic<int> next{0};
+  auto work = [&]() {
+    for (int g0; (g0 = next.fetch_add(32)) < n;)
+      for (int g = g0; g < std::min(n, g0 + 32); g++) f(g);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; t++) pool.emplace_back(work);
+  work();
+  for (auto &t : pool) t.join();
 }
 
-int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
-                         const int64_t *rp_off, const int32_t *rowptr, const int64_t *nz_off,
-                         const int32_t *col, const double *val, cfgsim_corpus **out) {
+// CSC of every graph (rows ascending within a column), same offsets as the
+// CSR; false if a column index is out of range
+bool build_csc(int32_t n_graphs, const int32_t *n_nodes, const int64_t *rp_off, const int32_t *rowptr,
+               const int64_t *nz_off, const int32_t *col, const double *val, int32_t *cscp, int32_t *crow,
+               double *cval, int &bad_graph) {
+  std::atomic<int> bad{-1};
+  parallel_graphs(n_graphs, [&](int g) {
+    const int n = n_nodes[g];
+    const int32_t *rp = rowptr + rp_off[g];
+    int32_t *cp = cscp + rp_off[g];
+    for (int k = 0; k <= n; k++) cp[k] = 0;
+    for (int r = 0; r < n; r++)
+      for (int32_t q = rp[r]; q < rp[r + 1]; q++) {
+        const int cc = col[nz_off[g] + q];
+        if (cc < 0 || cc >= n) {
+          int e = -1;
+          bad.compare_exchange_strong(e, g);
+          return;
+        }
+        cp[cc + 1]++;
+      }
+    for (int k = 0; k < n; k++) cp[k + 1] += cp[k];
+    std::vector<int32_t> fill(cp, cp + n);
+    for (int r = 0; r < n; r++)
+      for (int32_t q = rp[r]; q < rp[r + 1]; q++) {
+        const int cc = col[nz_off[g] + q];
+        const int32_t at = fill[cc]++;
+        crow[nz_off[g] + at] = r;
+        cval[nz_off[g] + at] = val[nz_off[g] + q];
+      }
+  });
+  bad_graph = bad.load();
+  return bad_graph < 0;
+}
+
+int corpus_create_impl(int32_t device, int32_t n_graphs, const int32_t *n_nodes, const int64_t *rp_off,
+                       const int32_t *rowptr, const int64_t *nz_off, const int32_t *col, const double *val,
+                       const int32_t *cscp_in, const int32_t *crow_in, const double *cval_in, cfgsim_corpus **out) {
   if (!out || n_graphs < 1 || !n_nodes || !rp_off || !rowptr || !nz_off)
     return fail(CFGSIM_ERR_ARG, "bad corpus arguments");
   if (int rc = set_device(device)) return rc;
@@ -1171,31 +1209,18 @@ int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_node
   if (e == cudaSuccess) e = up(c->d_nz_off, nz_off, sizeof(int64_t) * n_graphs);
   if (e == cudaSuccess) e = up(c->d_col, col, sizeof(int32_t) * nz_total);
   if (e == cudaSuccess) e = up(c->d_val, val, sizeof(double) * nz_total);
-  {  // CSC of every graph (rows ascending within a column), same offsets as the CSR
+  if (cscp_in) {  // prebuilt by the dense packer
+    if (e == cudaSuccess) e = up(c->d_cscp, cscp_in, sizeof(int32_t) * rp_total);
+    if (e == cudaSuccess) e = up(c->d_csc_row, crow_in, sizeof(int32_t) * nz_total);
+    if (e == cudaSuccess) e = up(c->d_csc_val, cval_in, sizeof(double) * nz_total);
+  } else {
     std::vector<int32_t> cscp(rp_total, 0), crow(nz_total, 0);
     std::vector<double> cval(nz_total, 0.0);
-    for (int g = 0; g < n_graphs; g++) {
-      const int n = n_nodes[g];
-      const int32_t *rp = rowptr + rp_off[g];
-      int32_t *cp = cscp.data() + rp_off[g];
-      for (int r = 0; r < n; r++)
-        for (int32_t q = rp[r]; q < rp[r + 1]; q++) {
-          const int cc = col[nz_off[g] + q];
-          if (cc < 0 || cc >= n) {
-            delete c;
-            return fail(CFGSIM_ERR_ARG, "column index out of range in graph " + std::to_string(g));
-          }
-          cp[cc + 1]++;
-        }
-      for (int k = 0; k < n; k++) cp[k + 1] += cp[k];
-      std::vector<int32_t> fill(cp, cp + n);
-      for (int r = 0; r < n; r++)
-        for (int32_t q = rp[r]; q < rp[r + 1]; q++) {
-          const int cc = col[nz_off[g] + q];
-          const int32_t at = fill[cc]++;
-          crow[nz_off[g] + at] = r;
-          cval[nz_off[g] + at] = val[nz_off[g] + q];
-        }
+    int bad = -1;
+    if (!build_csc(n_graphs, n_nodes, rp_off, rowptr, nz_off, col, val, cscp.data(), crow.data(), cval.data(),
+                   bad)) {
+      delete c;
+      return fail(CFGSIM_ERR_ARG, "column index out of range in graph " + std::to_string(bad));
     }
     if (e == cudaSuccess) e = up(c->d_cscp, cscp.data(), sizeof(int32_t) * rp_total);
     if (e == cudaSuccess) e = up(c->d_csc_row, crow.data(), sizeof(int32_t) * nz_total);
@@ -1212,35 +1237,83 @@ int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_node
   return CFGSIM_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+const char *cfgsim_last_error(void) { return g_err.c_str(); }
+int cfgsim_version(void) { return 100; }
+int64_t cfgsim_launch_count(void) { return g_launches.load(); }
+
+int cfgsim_device_count(int32_t *n) {
+  if (!n) return fail(CFGSIM_ERR_ARG, "n is NULL");
+  *n = 0;
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return CFGSIM_OK;
+  }
+  for (int i = 0; i < c; i++) {
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, i) == cudaSuccess && pr.major == 10) (*n)++;
+  }
+  return CFGSIM_OK;
+}
+
+int cfgsim_corpus_create(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
+                         const int64_t *rp_off, const int32_t *rowptr, const int64_t *nz_off,
+                         const int32_t *col, const double *val, cfgsim_corpus **out) {
+  return corpus_create_impl(device, n_graphs, n_nodes, rp_off, rowptr, nz_off, col, val, nullptr, nullptr, nullptr,
+                            out);
+}
+
 int cfgsim_corpus_create_dense(int32_t device, int32_t n_graphs, const int32_t *n_nodes, const double *const *mats,
                                cfgsim_corpus **out) {
   if (!out || n_graphs < 1 || !n_nodes || !mats) return fail(CFGSIM_ERR_ARG, "bad corpus arguments");
-  std::vector<int64_t> rp_off(n_graphs), nz_off(n_graphs);
-  std::vector<int32_t> rowptr, col;
-  std::vector<double> val;
-  int64_t rp_at = 0;
-  for (int g = 0; g < n_graphs; g++) {
+  for (int g = 0; g < n_graphs; g++)
+    if (n_nodes[g] < 1 || !mats[g]) return fail(CFGSIM_ERR_ARG, "graph with no nodes (EmptyGraph)");
+  // graph-parallel packing: nonzero counts, offsets, then CSR and CSC fills
+  std::vector<int64_t> nnz(n_graphs), rp_off(n_graphs), nz_off(n_graphs);
+  parallel_graphs(n_graphs, [&](int g) {
     const int n = n_nodes[g];
-    if (n < 1 || !mats[g]) return fail(CFGSIM_ERR_ARG, "graph with no nodes (EmptyGraph)");
-    rp_off[g] = rp_at;
-    nz_off[g] = (int64_t)col.size();
     const double *m = mats[g];
-    const size_t base = col.size();
-    rowptr.push_back(0);
+    int64_t k = 0;
+    for (size_t e = 0; e < (size_t)n * n; e++) k += m[e] != 0.0;
+    nnz[g] = k;
+  });
+  int64_t rp_at = 0, nz_at = 0;
+  for (int g = 0; g < n_graphs; g++) {
+    rp_off[g] = rp_at;
+    nz_off[g] = nz_at;
+    rp_at += n_nodes[g] + 1;
+    nz_at += nnz[g];
+  }
+  std::vector<int32_t> rowptr(rp_at), col(nz_at), cscp(rp_at), crow(nz_at);
+  std::vector<double> val(nz_at), cval(nz_at);
+  parallel_graphs(n_graphs, [&](int g) {
+    const int n = n_nodes[g];
+    const double *m = mats[g];
+    int32_t *rp = rowptr.data() + rp_off[g];
+    int32_t *cl = col.data() + nz_off[g];
+    double *vl = val.data() + nz_off[g];
+    int32_t k = 0;
+    rp[0] = 0;
     for (int r = 0; r < n; r++) {
       for (int q = 0; q < n; q++) {
         const double v = m[(size_t)r * n + q];
         if (v != 0.0) {
-          col.push_back(q);
-          val.push_back(v);
+          cl[k] = q;
+          vl[k++] = v;
         }
       }
-      rowptr.push_back((int32_t)(col.size() - base));
+      rp[r + 1] = k;
     }
-    rp_at += n + 1;
-  }
-  return cfgsim_corpus_create(device, n_graphs, n_nodes, rp_off.data(), rowptr.data(), nz_off.data(), col.data(),
-                              val.data(), out);
+  });
+  int bad = -1;
+  build_csc(n_graphs, n_nodes, rp_off.data(), rowptr.data(), nz_off.data(), col.data(), val.data(), cscp.data(),
+            crow.data(), cval.data(), bad);
+  return corpus_create_impl(device, n_graphs, n_nodes, rp_off.data(), rowptr.data(), nz_off.data(), col.data(),
+                            val.data(), cscp.data(), crow.data(), cval.data(), out);
 }
 
 int cfgsim_corpus_destroy(cfgsim_corpus *c) {
