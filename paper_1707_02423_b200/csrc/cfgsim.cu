@@ -604,15 +604,24 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
   pp.cbase = cbase;
   pp.cbase2 = cbase2;
   pp.apow = S.seq_apow.as<double>();
-  const int nt = 32 * (pw + 1);
   static const int minb_env = [] {  // CFGSIM_P2_OCC=2|3: CTAs/SM the stage-2 kernel is compiled for
     const char *e = getenv("CFGSIM_P2_OCC");
     return e ? atoi(e) : 3;
   }();
-  const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
-                                          : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
-                         : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
-                                          : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
+  static const int nc_env = [] {  // CFGSIM_P2_NC=1|2: consumer warps (greedy rounds) per stage-2 CTA;
+    const char *e = getenv("CFGSIM_P2_NC");  // 2 measured 2% slower on C2 (register pressure)
+    return e && atoi(e) == 2 ? 2 : 1;
+  }();
+  const int nt = 32 * (pw + nc_env);
+  const void *f2;
+  if (nc_env == 1)
+    f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4, 1>
+                                : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6, 1>)
+               : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2, 1>
+                                : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3, 1>);
+  else
+    f2 = small ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6, 2>
+               : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3, 2>;
   const size_t smem = p2_smem_bytes(N, sizeof(T));
   CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;

@@ -360,7 +360,7 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize) {
   s.amb = take(P2_MW * sizeof(uint32_t));
   s.item = take(sizeof(int64_t));
   s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
-  s.mrow = take(sizeof(int32_t) * 192);
+  s.mrow = take(sizeof(int32_t) * 192 * 2);  // per consumer warp: column, key hi, key lo
   s.tab = take(sizeof(double) * 3 * (P2_KMAX + 2));  // alpha^m, (T)(c alpha^m), (T)(alpha^m / N^2)
   s.total = o;
   return s;
@@ -713,8 +713,8 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
   return wsum;
 }
 
-template <typename T, int KB, int AR, int BC, int PW, int MINB>
-__global__ void __launch_bounds__(32 * (PW + 1), MINB)
+template <typename T, int KB, int AR, int BC, int PW, int MINB, int NC>
+__global__ void __launch_bounds__(32 * (PW + NC), MINB)
     isorank_pair2_kernel(const int32_t *n_nodes, PairWork work, PairOut out, Pair2Params prm, const T *useq,
                          const double *dseq, const int64_t *uoff, unsigned long long *counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -726,16 +726,19 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   int64_t *s_item = (int64_t *)(smem_raw + L.item);
   int32_t *s_first = (int32_t *)(smem_raw + L.first);
   constexpr int NP = 32 * PW;       // producer threads
-  constexpr int NALL = NP + 32;     // producers + consumer warp
+  constexpr int NALL = NP + 32;     // producers + the buffer's consumer warp
   constexpr int BAR_P = 1, BAR_FULL = 2, BAR_EMPTY = 4;  // named barriers (ids 2,3 / 4,5 per buffer)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double inv_nn = 1.0 / (double)((long long)N * N);
 
-  if (warp == PW) {
-    // ---------------- consumer: greedy rounds of the pairs in order
-    int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
-    for (int it = 0;; it++) {
+  if (warp >= PW) {
+    // ---------------- consumers: greedy rounds.  NC == 1: one warp takes the
+    // pairs in order, alternating buffers; NC == 2: consumer warp c owns
+    // buffer c (pairs of parity c), so two pairs' rounds run at once
+    const int cw = warp - PW;
+    int32_t *mrow = (int32_t *)(smem_raw + L.mrow) + 192 * cw;
+    for (int it = cw;; it += NC) {
       const int s = it & 1;
       nbar_sync(BAR_FULL + s, NALL);
       const P2Meta mt = meta[s];
@@ -785,7 +788,11 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     if (item >= work.n_items) {
       if (tid == 0) meta[s].valid = 0;
       nbar_arrive(BAR_FULL + s, NALL);
-      if (it >= 1) nbar_sync(BAR_EMPTY + (s ^ 1), NALL);  // match the consumer's last release
+      if (it >= 1) nbar_sync(BAR_EMPTY + (s ^ 1), NALL);  // match the release of pair it - 1
+      if (NC == 2) {  // the other consumer waits on buffer s ^ 1 for pair it + 1
+        if (tid == 0) meta[s ^ 1].valid = 0;
+        nbar_arrive(BAR_FULL + (s ^ 1), NALL);
+      }
       break;
     }
     T *Xs = (T *)(smem_raw + L.x[s]);
