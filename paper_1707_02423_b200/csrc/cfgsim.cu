@@ -623,7 +623,7 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
   else
     f2 = small ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6, 2>
                : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3, 2>;
-  const size_t smem = p2_smem_bytes(N, sizeof(T));
+  const size_t smem = p2_smem_bytes(N, sizeof(T), rr.kcap);
   CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f2, nt, smem));

@@ -339,7 +339,7 @@ struct P2Smem {
   size_t x[2], ord[2], meta, red, amb, item, first, mrow, tab, total;
 };
 
-__host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize) {
+__host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
   P2Smem s;
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -361,11 +361,14 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize) {
   s.item = take(sizeof(int64_t));
   s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
   s.mrow = take(sizeof(int32_t) * 192 * 2);  // per consumer warp: column, key hi, key lo
-  s.tab = take(sizeof(double) * 3 * (P2_KMAX + 2));  // alpha^m, (T)(c alpha^m), (T)(alpha^m / N^2)
+  s.tab = take(sizeof(double) * 3 * (kcap + 2));  // alpha^m, (T)(c alpha^m), (T)(alpha^m / N^2)
   s.total = o;
   return s;
 }
-__host__ __device__ inline size_t p2_smem_bytes(int N, int tsize) { return p2_smem_layout(N, tsize).total; }
+// (sized by kcap: at N = 55..61 this is what lets three CTAs share an SM)
+__host__ __device__ inline size_t p2_smem_bytes(int N, int tsize, int kcap) {
+  return p2_smem_layout(N, tsize, kcap).total;
+}
 
 // One row of X (pitch P) into ord[0..N): (value desc, column asc), the order
 // of np.argmax's first occurrence in similarity.py:103.  Exact: keys are
@@ -719,7 +722,7 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
                          const double *dseq, const int64_t *uoff, unsigned long long *counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = prm.N, P = N | 1;
-  const P2Smem L = p2_smem_layout(N, sizeof(T));
+  const P2Smem L = p2_smem_layout(N, sizeof(T), prm.kcap);
   P2Meta *meta = (P2Meta *)(smem_raw + L.meta);
   double *red = (double *)(smem_raw + L.red);
   uint32_t *amb = (uint32_t *)(smem_raw + L.amb);
@@ -764,7 +767,7 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
   const double invN = 1.0 / (double)N;
   const double c = (1.0 - prm.alpha) * inv_nn;
   const int mmax = prm.max_iter < prm.kcap ? prm.max_iter : prm.kcap;
-  double *apw = (double *)(smem_raw + L.tab), *cfa = apw + (P2_KMAX + 2), *cfk = cfa + (P2_KMAX + 2);
+  double *apw = (double *)(smem_raw + L.tab), *cfa = apw + (prm.kcap + 2), *cfk = cfa + (prm.kcap + 2);
   for (int m = tid; m <= prm.kcap + 1; m += NP) {  // the per-pair coefficients, once per CTA
     apw[m] = prm.apow[m];
     cfa[m] = (double)(T)(c * prm.apow[m]);       // c alpha^m   (the low-rank kernel's cak)
