@@ -608,21 +608,11 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
     const char *e = getenv("CFGSIM_P2_OCC");
     return e ? atoi(e) : 3;
   }();
-  static const int nc_env = [] {  // CFGSIM_P2_NC=1|2: consumer warps (greedy rounds) per stage-2 CTA;
-    const char *e = getenv("CFGSIM_P2_NC");  // 2 measured 2% slower on C2 (register pressure)
-    return e ? atoi(e) : 1;  // 3: two consumers for N <= 32 only
-  }();
-  const int nc = (nc_env == 2 || (nc_env == 3 && small)) ? 2 : 1;
-  const int nt = 32 * (pw + nc);
-  const void *f2;
-  if (nc == 1)
-    f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4, 1>
-                                : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6, 1>)
-               : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2, 1>
-                                : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3, 1>);
-  else
-    f2 = small ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6, 2>
-               : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3, 2>;
+  const int nt = 32 * (pw + 1);
+  const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
+                                          : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
+                         : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
+                                          : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
   const size_t smem = p2_smem_bytes(N, sizeof(T), rr.kcap);
   CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;

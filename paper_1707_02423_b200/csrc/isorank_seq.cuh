@@ -322,7 +322,6 @@ struct Pair2Params {
 // buffer, bar.sync / bar.arrive), so the sequential rounds overlap the GEMM
 // and sorts of the next pair.
 constexpr int P2_KC = 8;    // sweeps per staged chunk
-constexpr int P2_MW = 64;   // words of the ambiguous-sweep bitmask (kcap < 2048)
 constexpr int P2_KMAX = 512;  // kcap bound of the two-stage path (host checks)
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
@@ -356,16 +355,17 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
     s.ord[q] = take((size_t)N * N);    // row orders (columns, value desc / column asc)
   }
   s.meta = take(2 * sizeof(P2Meta));
-  s.red = take(32 * sizeof(double));
-  s.amb = take(P2_MW * sizeof(uint32_t));
+  s.red = take(8 * sizeof(double));  // one partial per producer warp
+  s.amb = take(((kcap >> 5) + 1) * sizeof(uint32_t));
   s.item = take(sizeof(int64_t));
   s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
-  s.mrow = take(sizeof(int32_t) * 192 * 2);  // per consumer warp: column, key hi, key lo
-  s.tab = take(sizeof(double) * 3 * (kcap + 2));  // alpha^m, (T)(c alpha^m), (T)(alpha^m / N^2)
+  s.mrow = take(sizeof(int32_t) * 128);  // the consumer's winners: column (value path) / key hi, lo
+  s.tab = take(sizeof(double) * (kcap + 2));  // alpha^m
   s.total = o;
   return s;
 }
-// (sized by kcap: at N = 55..61 this is what lets three CTAs share an SM)
+// (every region sized by N and kcap: 76.6 KB at N = 64, kcap = 137, so three
+// CTAs share an SM at every N <= 64)
 __host__ __device__ inline size_t p2_smem_bytes(int N, int tsize, int kcap) {
   return p2_smem_layout(N, tsize, kcap).total;
 }
@@ -687,9 +687,8 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
     const unsigned long long wk = __shfl_sync(0xffffffffu, mine, brow & 31);
     const int bcol = 63 - (int)(wk & 63ull);
     if (lane == 0) {
-      mrow[brow] = bcol;
-      mrow[64 + brow] = (int)(unsigned)(wk >> 32);  // winning key (value bits) for W
-      mrow[128 + brow] = (int)(unsigned)wk;
+      mrow[2 * brow] = (int)(unsigned)(wk >> 32);  // winning key (value bits) for W
+      mrow[2 * brow + 1] = (int)(unsigned)wk;
     }
     taken |= 1ull << bcol;
 #pragma unroll
@@ -710,14 +709,14 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
   __syncwarp();
   if (lane == 0)  // similarity.py:150: Python's sum, row order
     for (int i = 0; i < N; i++) {
-      const unsigned long long k = ((unsigned long long)(unsigned)mrow[64 + i] << 32) | (unsigned)mrow[128 + i];
+      const unsigned long long k = ((unsigned long long)(unsigned)mrow[2 * i] << 32) | (unsigned)mrow[2 * i + 1];
       wsum += p2_key_value<T>(k, emin);
     }
   return wsum;
 }
 
-template <typename T, int KB, int AR, int BC, int PW, int MINB, int NC>
-__global__ void __launch_bounds__(32 * (PW + NC), MINB)
+template <typename T, int KB, int AR, int BC, int PW, int MINB>
+__global__ void __launch_bounds__(32 * (PW + 1), MINB)
     isorank_pair2_kernel(const int32_t *n_nodes, PairWork work, PairOut out, Pair2Params prm, const T *useq,
                          const double *dseq, const int64_t *uoff, unsigned long long *counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -729,19 +728,17 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
   int64_t *s_item = (int64_t *)(smem_raw + L.item);
   int32_t *s_first = (int32_t *)(smem_raw + L.first);
   constexpr int NP = 32 * PW;       // producer threads
-  constexpr int NALL = NP + 32;     // producers + the buffer's consumer warp
+  constexpr int NALL = NP + 32;     // producers + consumer warp
   constexpr int BAR_P = 1, BAR_FULL = 2, BAR_EMPTY = 4;  // named barriers (ids 2,3 / 4,5 per buffer)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double inv_nn = 1.0 / (double)((long long)N * N);
 
-  if (warp >= PW) {
-    // ---------------- consumers: greedy rounds.  NC == 1: one warp takes the
-    // pairs in order, alternating buffers; NC == 2: consumer warp c owns
-    // buffer c (pairs of parity c), so two pairs' rounds run at once
-    const int cw = warp - PW;
-    int32_t *mrow = (int32_t *)(smem_raw + L.mrow) + 192 * cw;
-    for (int it = cw;; it += NC) {
+  if (warp == PW) {
+    // ---------------- consumer: greedy rounds of the pairs in order
+    // (a second consumer warp owning one buffer each measured 2% slower)
+    int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
+    for (int it = 0;; it++) {
       const int s = it & 1;
       nbar_sync(BAR_FULL + s, NALL);
       const P2Meta mt = meta[s];
@@ -767,12 +764,8 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
   const double invN = 1.0 / (double)N;
   const double c = (1.0 - prm.alpha) * inv_nn;
   const int mmax = prm.max_iter < prm.kcap ? prm.max_iter : prm.kcap;
-  double *apw = (double *)(smem_raw + L.tab), *cfa = apw + (prm.kcap + 2), *cfk = cfa + (prm.kcap + 2);
-  for (int m = tid; m <= prm.kcap + 1; m += NP) {  // the per-pair coefficients, once per CTA
-    apw[m] = prm.apow[m];
-    cfa[m] = (double)(T)(c * prm.apow[m]);       // c alpha^m   (the low-rank kernel's cak)
-    cfk[m] = (double)(T)(prm.apow[m] * inv_nn);  // alpha^m/N^2 (its sc)
-  }
+  double *apw = (double *)(smem_raw + L.tab);
+  for (int m = tid; m <= prm.kcap + 1; m += NP) apw[m] = prm.apow[m];  // alpha^m, once per CTA
   nbar_sync(BAR_P, NP);
   const int NPt = seq_pitch<T>(N);                      // history row pitch
   const int SPD = ((2 * NPt + 7) / 16) * 16 + 8;        // staged row pitch (== 8 mod 16 doubles: 2-wavefront fragments)
@@ -784,18 +777,14 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
       s_first[1] = 0x7fffffff;
       s_first[2] = -1;
     }
-    for (int q = tid; q < P2_MW; q += NP) amb[q] = 0u;
+    for (int q = tid; q <= (prm.kcap >> 5); q += NP) amb[q] = 0u;
     nbar_sync(BAR_P, NP);
     const int64_t item = *s_item;
     if (it >= 2) nbar_sync(BAR_EMPTY + s, NALL);  // buffer s released by the consumer (pair it-2)
     if (item >= work.n_items) {
       if (tid == 0) meta[s].valid = 0;
       nbar_arrive(BAR_FULL + s, NALL);
-      if (it >= 1) nbar_sync(BAR_EMPTY + (s ^ 1), NALL);  // match the release of pair it - 1
-      if (NC == 2) {  // the other consumer waits on buffer s ^ 1 for pair it + 1
-        if (tid == 0) meta[s ^ 1].valid = 0;
-        nbar_arrive(BAR_FULL + (s ^ 1), NALL);
-      }
+      if (it >= 1) nbar_sync(BAR_EMPTY + (s ^ 1), NALL);  // match the consumer's last release
       break;
     }
     T *Xs = (T *)(smem_raw + L.x[s]);
@@ -884,7 +873,7 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
           if (apw[m] * inv_nn * S < prm.tol) {  // similarity.py:144
             K = m;
             conv = true;
-            wd = P2_MW;
+            wd = prm.kcap;  // ends the scan
             break;
           }
         }
@@ -941,7 +930,8 @@ __global__ void __launch_bounds__(32 * (PW + NC), MINB)
         for (int k0 = 0; k0 < P2_KC; k0 += 4) {
           const int m = m0 + k0 + lk;  // this lane's k
           if (m0 + k0 > K) break;
-          const double cf = (m < K) ? cfa[m] : (m == K ? cfk[m] : 0.0);
+          // c alpha^m (the low-rank kernel's cak) / alpha^K / N^2 (its sc), rounded to T
+          const double cf = (m < K) ? (double)(T)(c * apw[m]) : (m == K ? (double)(T)(apw[m] * inv_nn) : 0.0);
           const T *row = buf + (k0 + lk) * SPD;
           double af[TR], bf[TC];
 #pragma unroll

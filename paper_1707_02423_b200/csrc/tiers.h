@@ -50,13 +50,12 @@
 // KB = sort chunks per lane: N <= 32 * KB
 #define CFGSIM_BIG_LIST_T(T, X) X(T, 8) X(T, 16) X(T, 32)
 
-// two-stage pair kernels: (T, KB, AR, BC, producer warps, MINB, consumer warps)
+// two-stage pair kernels: (T, KB, AR, BC, producer warps, MINB)
 #define CFGSIM_P2_LIST(X) \
-  X(double, 1, 4, 4, 2, 4, 1) X(double, 2, 4, 8, 4, 2, 1) X(float, 1, 4, 4, 2, 4, 1) X(float, 2, 4, 8, 4, 2, 1) \
-  X(double, 2, 4, 8, 4, 3, 1) X(float, 2, 4, 8, 4, 3, 1) X(double, 1, 4, 4, 2, 6, 1) X(float, 1, 4, 4, 2, 6, 1) \
-  X(double, 2, 4, 8, 4, 3, 2) X(float, 2, 4, 8, 4, 3, 2) X(double, 1, 4, 4, 2, 6, 2) X(float, 1, 4, 4, 2, 6, 2)
-#define CFGSIM_EXTERN_P2(T, KB, AR, BC, PW, MINB, NC)                                               \
-  extern template __global__ void cfgsim::isorank_pair2_kernel<T, KB, AR, BC, PW, MINB, NC>(       \
+  X(double, 1, 4, 4, 2, 4) X(double, 2, 4, 8, 4, 2) X(float, 1, 4, 4, 2, 4) X(float, 2, 4, 8, 4, 2) \
+  X(double, 2, 4, 8, 4, 3) X(float, 2, 4, 8, 4, 3) X(double, 1, 4, 4, 2, 6) X(float, 1, 4, 4, 2, 6)
+#define CFGSIM_EXTERN_P2(T, KB, AR, BC, PW, MINB)                                                   \
+  extern template __global__ void cfgsim::isorank_pair2_kernel<T, KB, AR, BC, PW, MINB>(           \
       const int32_t *, cfgsim::PairWork, cfgsim::PairOut, cfgsim::Pair2Params, const T *, const double *, \
       const int64_t *, unsigned long long *);
 
