@@ -23,6 +23,9 @@
 // Per pair this removes every sweep barrier and mat-vec: what remains is
 // ~K N^2 mma work, one sort per row and N greedy rounds.
 #pragma once
+#ifdef CFGSIM_DEBUG_SEQ4
+#include <cstdio>
+#endif
 #include "isorank_lr.cuh"
 #include "isorank_big.cuh"
 
@@ -229,6 +232,17 @@ __global__ void __launch_bounds__(32 * SEQ4) isorank_seq4_kernel(DevCorpus C, Se
       const int32_t *toff = (const int32_t *)(smem_raw + L.toff) + warp * (nl + 1);
       const int32_t *zl = (const int32_t *)(smem_raw + L.z) + warp * (nl + 1);
       const int nzv = nzs[4 * warp];
+#ifdef CFGSIM_DEBUG_SEQ4
+      if (lane == 0) {
+        const int ntot = toff[N];
+        bool bad = N > nl || N < 1 || ntot > prm.cap || ntot < 0 || nzv < 0 || nzv > N;
+        for (int t = 0; t < N && !bad; t++) bad = toff[t + 1] < toff[t];
+        for (int e = 0; e < ntot && e < prm.cap && !bad; e++) bad = idx[e] < 0 || idx[e] >= N;
+        if (bad)
+          printf("seq4 bad list: block %d warp %d combo %lld g %d N %d n %d toff[N] %d cap %d nzv %d ok %d\n",
+                 blockIdx.x, warp, (long long)c, cb.g[c], N, C.n_nodes[cb.g[c]], ntot, prm.cap, nzv, nzs[4 * warp + 1]);
+      }
+#endif
       T *u = (T *)(smem_raw + L.u) + (size_t)warp * 2 * nl;
       const T invN = (T)(1.0 / (double)N);
       const int NPt = seq_pitch<T>(N);
