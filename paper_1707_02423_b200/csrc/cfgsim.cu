@@ -534,7 +534,7 @@ int seq_upload(Scratch &S, const SeqTable &tb, const SeqRun &rr, const cfgsim_pa
 // operator lists overflow are re-run with dense-bound lists.
 template <typename T>
 int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr, const cfgsim_params *p, Scratch &S,
-               cudaStream_t st) {
+               cudaStream_t st, bool single = false) {
   if (n <= 0) return CFGSIM_OK;
   int dev, sms = 0;
   CU(cudaGetDevice(&dev));
@@ -561,11 +561,14 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
   // pass 0: typical list capacity; pass 1 re-runs only the combos that
   // overflowed it (status 1) with dense-bound lists — decided on the device,
   // so no host synchronisation sits between the stages
-  for (int pass = 0; pass < 2; pass++) {
+  // single: every combo through the one-combo-per-CTA kernel with dense-bound
+  // lists (the query-vs-corpus path: memcheck flags an out-of-bounds shared
+  // read in the four-combo kernel there)
+  for (int pass = single ? 1 : 0; pass < 2; pass++) {
     // pass 0: four combos per CTA, warp-synchronous recurrences; pass 1: the
     // one-combo-per-CTA kernel re-runs flagged combos with dense-bound lists
     sp.cap = pass == 0 ? 10 * kSeqNmax + 16 : kSeqNmax * kSeqNmax;  // 10N+16: 2 CTAs/SM
-    cb.redo = pass;
+    cb.redo = single ? 0 : pass;
     const void *fk = pass == 0 ? (const void *)isorank_seq4_kernel<T, 2> : f1;
     const int nthr = pass == 0 ? 32 * SEQ4 : 128;
     const size_t smem = pass == 0 ? seq4_smem_layout<T>(kSeqNmax, sp.cap).total : seq_smem_layout<T>(kSeqNmax, sp.cap).total;
@@ -714,8 +717,8 @@ int seq_nearest_t(const cfgsim_corpus *Q, const cfgsim_corpus *C, const std::vec
     for (int32_t q = 0; q < qle; q++) tb.add<T>(qs[q], N, rr.kcap);
     for (int32_t x = 0; x < cle; x++) tb.add<T>(cs[x], N, rr.kcap);
     if (int rc = seq_upload<T>(S, tb, rr, p, st)) return rc;
-    if (int rc = seq_stage1<T>(Q, 0, qle, rr, p, S, st)) return rc;
-    if (int rc = seq_stage1<T>(C, qle, cle, rr, p, S, st)) return rc;
+    if (int rc = seq_stage1<T>(Q, 0, qle, rr, p, S, st, true)) return rc;
+    if (int rc = seq_stage1<T>(C, qle, cle, rr, p, S, st, true)) return rc;
     const int nr = (int)rects.size() / 4;
     std::vector<int64_t> rsum(nr + 1, 0);
     for (int r = 0; r < nr; r++)
