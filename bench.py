@@ -111,7 +111,7 @@ def cpu_sample(mats, seconds, seed=0, queries=None):
     """C restatement of the reference (oracle/, pthreads over all host cores) on
     a random sample of the workload's pairs, grown until `seconds`."""
     from oracle import ffi
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
     threads = os.cpu_count() or 1
     allm = (queries or []) + list(mats)
     packed = pack(allm)

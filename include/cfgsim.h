@@ -17,6 +17,16 @@
  *    stream-ordered and asynchronous.
  *  - results are bitwise deterministic: independent of stream, launch
  *    order, tile, grid size or device count.
+ *  - threading: any host thread may call any function.  The library keeps
+ *    per-device scratch (work counters, overflow lists, combo tables) shared
+ *    by all handles on that device; calls that use it are serialised per
+ *    device (a mutex for host threads, plus an event so a call's stream
+ *    waits for the previous call's stream work).  A corpus handle is
+ *    read-only after creation and may be used by several threads; destroy
+ *    it only after every call using it has returned and its stream work
+ *    has completed.  While a stream is being captured into a CUDA graph the
+ *    cross-stream event ordering is skipped: replay the graph on one stream
+ *    (or order it yourself) against other library calls.
  *
  * Packed corpus (CSR of the raw TransitionMatrix.entries, matrix.py:24-42):
  *  graph g has n_nodes[g] rows; its row pointer is

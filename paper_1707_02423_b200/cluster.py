@@ -16,11 +16,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _native as nat
-from .errors import DimMismatch, SasscfgError
-
-
-class BadK(SasscfgError):
-    """Cluster count outside 1..n (cluster.py:140-141)."""
+from .errors import BadK, DimMismatch
 
 
 @dataclass(frozen=True)
@@ -81,18 +77,35 @@ def ward_linkage(vectors: Sequence[FeatureVector], *, device: int | None = None)
 
 
 def cut_clusters(linkage: Linkage, k: int, ids: Sequence[str]) -> dict[str, int]:
-    """The clusters left after n - k merges, indexed by their smallest leaf
-    (cluster.py:137-154)."""
+    """Flat clustering after the first n - k merges (cluster.py:130-145):
+    cluster indices are assigned in increasing order of each cluster's
+    smallest leaf.
+
+    Union-find over the leaves: merged cluster n + s owns the representative
+    of its two parts, so each merge is two finds and one link."""
     n = linkage.n_leaves
     if not 1 <= k <= n:
         raise BadK(f"cluster count {k} outside 1..{n}")
     if len(ids) != n:
         raise DimMismatch(f"{len(ids)} ids for {n} leaves")
-    members: dict[int, list[int]] = {i: [i] for i in range(n)}
-    for step, (a, b, _d, _s) in enumerate(linkage.merges[: n - k]):
-        members[n + step] = members.pop(a) + members.pop(b)
-    groups = sorted(members.values(), key=min)
-    return {ids[leaf]: index for index, leaves in enumerate(groups) for leaf in leaves}
+    parent = list(range(n))
+    rep = list(range(n)) + [0] * (n - 1)  # cluster id -> one leaf of it
+
+    def find(x: int) -> int:
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for s in range(n - k):
+        a, b = linkage.merges[s][0], linkage.merges[s][1]
+        ra, rb = find(rep[a]), find(rep[b])
+        lo, hi = (ra, rb) if ra < rb else (rb, ra)
+        parent[hi] = lo  # the root is always the smallest leaf of its cluster
+        rep[n + s] = lo
+    roots = sorted({find(x) for x in range(n)})
+    index = {r: i for i, r in enumerate(roots)}
+    return {ids[x]: index[find(x)] for x in range(n)}
 
 
 def export_linkage_csv(linkage: Linkage) -> str:

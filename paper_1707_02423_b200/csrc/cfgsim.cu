@@ -209,11 +209,20 @@ int cap_for(int precision, const Plan &pl, int nlim, bool dense) {
   return std::max(1, std::min(dc, (int)((budget - base) / (2 * T.entry_bytes)) - 8));
 }
 
+// Per-device scratch shared by every corpus handle on that device (work
+// counters, overflow lists, large-N slabs, two-stage combo tables).  Calls
+// that use it are serialised per device (DeviceGuard below): a recursive
+// mutex for host threads, and an event recorded on the previous user's stream
+// that the next user's stream waits on, so async calls on different streams
+// never overlap on the shared buffers.
 struct Scratch {
   DBuf counters, ovf_count, ovf_list, gslab, status;
   DBuf seq_u, seq_d, seq_g, seq_n, seq_off, seq_st, seq_list, seq_apow;  // two-stage combos
   std::string seq_key;  // identity of the combo tables currently uploaded ("" = none)
   int64_t ovf_cap = 0;
+  std::recursive_mutex mu;
+  cudaEvent_t done = nullptr;  // recorded at the end of the last call's stream work
+  int depth = 0;               // nesting of guards on the owning thread
 };
 
 Scratch &scratch_for(int device) {
@@ -223,6 +232,42 @@ Scratch &scratch_for(int device) {
   if (!per_dev[device]) per_dev[device] = new Scratch();
   return *per_dev[device];
 }
+
+// Serialises one ABI call's use of the device's Scratch (see Scratch).  While
+// a stream is being captured into a CUDA graph the event wait/record is
+// skipped (graph replays are ordered by the capturing stream itself).
+class DeviceGuard {
+ public:
+  DeviceGuard(int device, cudaStream_t st) : S_(scratch_for(device)), st_(st), lk_(S_.mu) {
+    if (S_.depth++ > 0) return;  // nested call: the outermost guard orders the stream
+    capturing_ = is_capturing(st);
+    if (!S_.done && cudaEventCreateWithFlags(&S_.done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      S_.done = nullptr;
+    }
+    if (S_.done && !capturing_) cudaStreamWaitEvent(st_, S_.done, 0);
+  }
+  ~DeviceGuard() {
+    if (--S_.depth > 0) return;
+    if (S_.done && !capturing_) cudaEventRecord(S_.done, st_);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+
+ private:
+  static bool is_capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return cs != cudaStreamCaptureStatusNone;
+  }
+  Scratch &S_;
+  cudaStream_t st_;
+  std::lock_guard<std::recursive_mutex> lk_;
+  bool capturing_ = false;
+};
 
 // Launch one tier over `work` (persistent grid, atomic work counter).
 int launch_tier(int precision, int ti, int nlim, int cap, const DevCorpus &A, const DevCorpus &B,
@@ -562,8 +607,7 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
   // overflowed it (status 1) with dense-bound lists — decided on the device,
   // so no host synchronisation sits between the stages
   // single: every combo through the one-combo-per-CTA kernel with dense-bound
-  // lists (the query-vs-corpus path: memcheck flags an out-of-bounds shared
-  // read in the four-combo kernel there)
+  // lists (A/B and debugging; CFGSIM_SEQ_SINGLE=1)
   for (int pass = single ? 1 : 0; pass < 2; pass++) {
     // pass 0: four combos per CTA, warp-synchronous recurrences; pass 1: the
     // one-combo-per-CTA kernel re-runs flagged combos with dense-bound lists
@@ -717,8 +761,8 @@ int seq_nearest_t(const cfgsim_corpus *Q, const cfgsim_corpus *C, const std::vec
     for (int32_t q = 0; q < qle; q++) tb.add<T>(qs[q], N, rr.kcap);
     for (int32_t x = 0; x < cle; x++) tb.add<T>(cs[x], N, rr.kcap);
     if (int rc = seq_upload<T>(S, tb, rr, p, st)) return rc;
-    if (int rc = seq_stage1<T>(Q, 0, qle, rr, p, S, st, true)) return rc;
-    if (int rc = seq_stage1<T>(C, qle, cle, rr, p, S, st, true)) return rc;
+    if (int rc = seq_stage1<T>(Q, 0, qle, rr, p, S, st)) return rc;
+    if (int rc = seq_stage1<T>(C, qle, cle, rr, p, S, st)) return rc;
     const int nr = (int)rects.size() / 4;
     std::vector<int64_t> rsum(nr + 1, 0);
     for (int r = 0; r < nr; r++)
@@ -1322,7 +1366,9 @@ int cfgsim_corpus_create_dense(int32_t device, int32_t n_graphs, const int32_t *
 int cfgsim_corpus_destroy(cfgsim_corpus *c) {
   if (c) {
     cudaSetDevice(c->device);
-    scratch_for(c->device).seq_key.clear();  // a new corpus may reuse this address
+    Scratch &S = scratch_for(c->device);
+    std::lock_guard<std::recursive_mutex> lk(S.mu);
+    S.seq_key.clear();  // a new corpus may reuse this address
     delete c;
   }
   return CFGSIM_OK;
@@ -1346,6 +1392,7 @@ int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t
   if (A->device != B->device) return fail(CFGSIM_ERR_ARG, "corpora live on different devices");
   if (int rc = set_device(A->device)) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  DeviceGuard guard(A->device, st);
   std::vector<int32_t> ha(n_pairs), hb(n_pairs);
   if (n_pairs) {
     CU(cudaMemcpyAsync(ha.data(), ia, sizeof(int32_t) * n_pairs, cudaMemcpyDefault, st));
@@ -1411,6 +1458,7 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   if ((d_lin && !is_device_ptr(d_lin)) || (iters_lin && !is_device_ptr(iters_lin)))
     return fail(CFGSIM_ERR_ARG, "allpairs_range outputs must be device pointers");
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  DeviceGuard guard(c->device, st);
   Scratch &S = scratch_for(c->device);
   if (int rc = ensure_scratch(S, 1 << 16)) return rc;
   const bool lr = use_lowrank();
@@ -1514,6 +1562,7 @@ int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params
   if (int rc = check_params(p)) return rc;
   if (int rc = set_device(c->device)) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  DeviceGuard guard(c->device, st);
   const int64_t nu = c->row_start[c->K];
   const int64_t slots = ordered ? 2 * nu : nu;
   DBuf dl, il;
@@ -1541,6 +1590,7 @@ int cfgsim_isorank_single(int32_t device, int32_t na, const double *A, int32_t n
   if (na < 1 || nb < 1 || !A || !B) return fail(CFGSIM_ERR_ARG, "bad matrices");
   if (int rc = check_params(p)) return rc;
   if (int rc = set_device(device)) return rc;
+  DeviceGuard guard(device, 0);
   cfgsim_corpus *ca = nullptr, *cb = nullptr;
   if (int rc = corpus_from_dense(device, na, A, &ca)) return rc;
   if (int rc = corpus_from_dense(device, nb, B, &cb)) {
@@ -1593,6 +1643,7 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
   if (Q->device != C->device) return fail(CFGSIM_ERR_ARG, "corpora live on different devices");
   if (int rc = set_device(Q->device)) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  DeviceGuard guard(Q->device, st);
   const int32_t nq = Q->K, nc = c1 - c0;
   OutStage sd, si;
   CU(sd.prepare(best_d, sizeof(double) * nq));

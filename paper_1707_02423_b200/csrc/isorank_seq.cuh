@@ -272,7 +272,10 @@ __global__ void __launch_bounds__(32 * SEQ4) isorank_seq4_kernel(DevCorpus C, Se
         const int t0 = lane, t1 = lane + 32;
         T a0 = zt, a1 = 0, b0 = zt, b1 = 0;
         {
-          int e = toff[t0], e1 = t0 < N ? toff[t0 + 1] : e;
+          // only live rows read their list offsets: slots past N hold whatever
+          // an earlier kernel left in shared memory (e.g. the stage-2 kernel's
+          // 0x7fffffff sentinels), and e + 1 < e1 must never see them
+          int e = t0 < N ? toff[t0] : 0, e1 = t0 < N ? toff[t0 + 1] : 0;
           int f = t1 < N ? toff[t1] : 0, f1 = t1 < N ? toff[t1 + 1] : 0;
           while (e + 1 < e1 || f + 1 < f1) {
             if (e + 1 < e1) {
@@ -530,6 +533,13 @@ __device__ __forceinline__ unsigned long long p2_key(T v, int col, int emin) {
   } else {
     return ((unsigned long long)__float_as_uint((float)v) << 6) | (unsigned long long)(63 - col);
   }
+}
+// X is stored as packed keys when they are exact: always for fp32 (the float
+// bits themselves), for fp64 when the pair's exponent span fits the 6-bit
+// field; otherwise as values (p2_sort_row's value path)
+template <typename T>
+__device__ __forceinline__ bool p2_use_keys(int emin, int emax) {
+  return sizeof(T) == 4 || (emax - emin < 64);
 }
 template <typename T>
 __device__ __forceinline__ double p2_key_value(unsigned long long k, int emin) {
@@ -989,7 +999,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       }
       nbar_sync(BAR_P, NP);
       const int emin = s_first[1];
-      const bool keys = s_first[2] - emin < 64;
+      const bool keys = p2_use_keys<T>(emin, s_first[2]);  // the same predicate as the readers below
       constexpr int PK = 32 * KB + 1;
       unsigned long long *Kr = (unsigned long long *)Xs;
 #pragma unroll
@@ -1007,7 +1017,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     }
     nbar_sync(BAR_P, NP);
     const int emin = s_first[1];
-    const bool keys = sizeof(T) == 4 || (s_first[2] - emin < 64);
+    const bool keys = p2_use_keys<T>(emin, s_first[2]);
     constexpr int PK = 32 * KB + 1;
     unsigned long long *Kr = (unsigned long long *)Xs;
     if (keys) {

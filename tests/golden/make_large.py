@@ -29,7 +29,7 @@ sys.path.insert(0, str(REPO))
 
 from oracle import ffi  # noqa: E402
 from paper_1707_02423_b200 import synth  # noqa: E402
-from paper_1707_02423_b200.corpus import pack  # noqa: E402
+from paper_1707_02423_b200.packing import pack  # noqa: E402
 
 
 def cfg(rng, n, weighting):

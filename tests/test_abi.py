@@ -58,7 +58,7 @@ def test_no_cpu_fallback_without_gpu():
 
 
 def test_pack_layout():
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
     a = np.array([[0.0, 0.5], [1.0, 0.0]])
     b = np.array([[0.25, 0.0, 0.75], [0.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
     p = pack([a, b])

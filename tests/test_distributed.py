@@ -57,7 +57,7 @@ def _worker(rank, world, port, out_path):
     sys.path.insert(0, str(REPO))
     from oracle import ffi
     from paper_1707_02423_b200 import synth
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
     from paper_1707_02423_b200.distributed import allpairs_sharded, unit_pairs
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -83,7 +83,7 @@ def test_gloo_world2_matches_single_rank(tmp_path):
     sys.path.insert(0, str(REPO))
     from oracle import ffi
     from paper_1707_02423_b200 import synth
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
 
     out = tmp_path / "m.npy"
     mp.start_processes(_worker, args=(2, _free_port(), str(out)), nprocs=2, start_method="spawn")
@@ -113,7 +113,7 @@ def _nearest_worker(rank, world, port, out_path):
     sys.path.insert(0, str(REPO))
     from oracle import ffi
     from paper_1707_02423_b200 import synth
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
     from paper_1707_02423_b200.distributed import nearest_sharded
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -145,7 +145,7 @@ def test_gloo_world2_nearest_matches_single_rank(tmp_path):
     sys.path.insert(0, str(REPO))
     from oracle import ffi
     from paper_1707_02423_b200 import synth
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
 
     out = tmp_path / "n.npy"
     mp.start_processes(_nearest_worker, args=(2, _free_port(), str(out)), nprocs=2, start_method="spawn")

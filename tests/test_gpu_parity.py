@@ -390,3 +390,22 @@ def test_allpairs_parameters_match_oracle(P, alpha, tol, max_iter):
                                  max_iter=max_iter)
     np.testing.assert_array_equal(iters[iu, ju], it)
     np.testing.assert_allclose(pm.scores[iu, ju], d, rtol=RTOL64)
+
+
+def test_nearest_small_queries_after_stage2(P):
+    """Regression (r1 memcheck finding): query-vs-corpus over graphs below 32
+    blocks right after a stage-2 launch, whose shared-memory sentinels used to
+    leak into the four-combo stage-1 kernel's list offsets for lanes >= N.
+    The rectangle path must equal the per-pair list path bitwise."""
+    from paper_1707_02423_b200 import synth
+    warm = synth.random_corpus(24, 16, 64, seed=9)
+    P.pairwise([P.TransitionMatrix(f"w{i:03d}.s.w", m, tuple(range(len(m))), P.ROW_STOCHASTIC)
+                for i, m in enumerate(warm)], P.MeasureId.ISO)
+    q = synth.random_corpus(96, 4, 31, seed=3)
+    c = synth.random_corpus(2500, 4, 31, seed=2)
+    bd, bi = P.nearest(q, c)
+    with P.DeviceCorpus(q) as CQ, P.DeviceCorpus(c) as CC:
+        dl, *_ = P.isorank_pairs(CQ, CC, np.repeat(np.arange(len(q)), len(c)), np.tile(np.arange(len(c)), len(q)))
+    dl = dl.reshape(len(q), len(c))
+    np.testing.assert_array_equal(bd, dl.min(axis=1))
+    np.testing.assert_array_equal(bi, dl.argmin(axis=1))

@@ -79,7 +79,7 @@ def test_survey_golden_row():
 def test_c_oracle_batch_matches_single():
     g = load_golden("synth_pairs.npz")
     mats = unravel(g["sa"], g["fa"])[:8] + unravel(g["sb"], g["fb"])[:8]
-    from paper_1707_02423_b200.corpus import pack
+    from paper_1707_02423_b200.packing import pack
     packed = pack(mats)
     ia = np.arange(8, dtype=np.int32)
     ib = ia + 8
