@@ -42,6 +42,7 @@ import numpy as np
 
 REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
+REF_SITE = REPO / "baseline" / "_ref"  # the unmodified reference (pip install --target, git-ignored)
 
 METRIC = "CFG-pair similarities/sec (IsoRank, device-timed)"
 UNIT = "pairs/s"
@@ -65,6 +66,7 @@ def parse():
     ap.add_argument("--queries", type=int, default=None, help="override query count (c3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=6.0, help="wall budget of the CPU sample")
     return ap.parse_args()
 
@@ -134,6 +136,79 @@ def cpu_sample(mats, seconds, seed=0, queries=None):
     return done / t_total, threads, done, t_total
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_worker_init():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    sys.path.insert(0, str(REF_SITE))
+
+
+def _ref_pair(job):
+    """Unmodified reference: sasscfg.similarity.measure_distance(a, b, ISO)."""
+    from sasscfg.matrix import ROW_STOCHASTIC, TransitionMatrix
+    from sasscfg.similarity import MeasureId, measure_distance
+    a, b = job
+    ta = TransitionMatrix("a.synth.ref.k", a, tuple(range(len(a))), ROW_STOCHASTIC)
+    tb = TransitionMatrix("b.synth.ref.k", b, tuple(range(len(b))), ROW_STOCHASTIC)
+    t0 = time.perf_counter()
+    d = measure_distance(ta, tb, MeasureId.ISO)
+    return d, time.perf_counter() - t0
+
+
+def reference_python_sample(mats, queries, seconds, nmax=96):
+    """The unmodified reference (baseline/_ref) on random pairs
+    of the workload: one process per core, OPENBLAS_NUM_THREADS=1, pairs
+    handed out in rounds until `seconds` of wall time.  Pairs with
+    N = max(n_a, n_b) > nmax are excluded (the reference's Kronecker matrix is
+    8 N^4 bytes: 34 GB at N = 256); the sample then covers only that slice."""
+    import multiprocessing as mp
+    if not (REF_SITE / "sasscfg").is_dir():
+        return {"unavailable": "baseline/_ref not installed"}
+    procs = os.cpu_count() or 1
+    rng = np.random.default_rng(5)
+    pool_a = list(queries) if queries else list(mats)
+    ok = [i for i in range(len(mats)) if len(mats[i]) <= nmax]
+    oka = [i for i in range(len(pool_a)) if len(pool_a[i]) <= nmax]
+    if not ok or not oka:
+        return {"unavailable": f"no pairs with N <= {nmax} in this workload (reference Kronecker is 8 N^4 bytes)"}
+    done, busy = 0, 0.0
+    # the spawned workers import numpy (bench.py's top level) before any
+    # initializer runs: single-threaded BLAS has to come from the environment
+    saved = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
+    os.environ.update({k: "1" for k in saved})
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs, initializer=_ref_worker_init) as pool:
+        pool.map(_ref_pair, [(mats[ok[0]], mats[ok[0]])] * procs)  # import sasscfg in every worker
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            jobs = [(pool_a[oka[int(rng.integers(len(oka)))]], mats[ok[int(rng.integers(len(ok)))]])
+                    for _ in range(procs)]
+            res = pool.map(_ref_pair, jobs)
+            done += len(jobs)
+            busy += sum(t for _, t in res)
+        wall = time.perf_counter() - t0
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+    full = len(ok) == len(mats) and len(oka) == len(pool_a)
+    return {"value": done / wall, "unit": UNIT, "cores": procs, "kind": "reference",
+            "sample": f"{done} random pairs of this workload{'' if full else f' with N <= {nmax}'}, "
+                      f"{wall:.1f} s wall on {procs} processes (mean {busy / max(done, 1):.3f} s/pair/core); "
+                      "unmodified sasscfg.similarity.measure_distance(a, b, ISO) from baseline/_ref, "
+                      "OPENBLAS_NUM_THREADS=1"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -160,6 +235,10 @@ def run_reference(args):
                                        f"(~{per_step:.0f} s each); C restatement of sasscfg isorank "
                                        "(oracle/isorank_ref.c, pinned to reference golden vectors)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line["cpu_baseline"]["cpu_model"] = cpu_model()
+    if args.config != "c4":
+        # second stated baseline: the unmodified Python reference itself
+        line["reference_python"] = reference_python_sample(mats, queries, seconds=15.0)
     print(json.dumps(line), flush=True)
 
 
@@ -228,6 +307,71 @@ class Clocks:
         loaded = [c for c in sm if c > 0.5 * (mx or 1)] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def parity_check(args, mats, queries, d_units=None, it_units=None, ga=None, gb=None, best=None, c0=0, c1=None):
+    """Parity of the benched step's own outputs against the pinned CPU oracle
+    (oracle/isorank_ref.c — the checker, run after the timed region).
+
+    All-pairs: >= 4,096 random units of this rank's range (time-boxed for the
+    large-N configs, whose oracle pairs take ~0.1-1 s each): identical
+    iteration counts, max relative error of d.  c3: 4,096 random (query,
+    corpus) pairs through the per-pair API (bitwise equal to the rectangle
+    path, tests/test_gpu_parity.py) plus the best match of sampled queries
+    over the whole corpus shard against the oracle's argmin."""
+    from oracle import ffi
+    from paper_1707_02423_b200.packing import pack
+    threads = os.cpu_count() or 1
+    budget = float(os.environ.get("CFGSIM_PARITY_SECONDS", "20"))
+    rng = np.random.default_rng(12345)
+    t_start = time.perf_counter()
+    if args.config != "c3":
+        packed = pack(mats)
+        n = len(d_units)
+        order = rng.permutation(n)
+        pairs = mism = 0
+        worst = 0.0
+        batch = 4096 if args.config == "c2" else max(threads, 16)
+        at = 0
+        while at < n and (pairs < 4096 if args.config == "c2" else time.perf_counter() - t_start < budget):
+            sel = order[at:at + batch]
+            at += len(sel)
+            a, b = np.minimum(ga[sel], gb[sel]), np.maximum(ga[sel], gb[sel])
+            d, _, it, _ = ffi.iso_batch(packed, a.astype(np.int32), b.astype(np.int32), threads=threads)
+            mism += int((it != it_units[sel]).sum())
+            worst = max(worst, float(np.max(np.abs(d_units[sel] - d) / d)))
+            pairs += len(sel)
+            batch = max(threads, 16) if args.config != "c2" else 4096
+        return {"checked": "this step's unit outputs vs oracle/isorank_ref.c", "pairs": pairs,
+                "iter_mismatches": mism, "max_rel_err": worst, "tolerance": 1e-9 if args.precision == "fp64" else 1e-5,
+                "sample": "uniform random units" + ("" if args.config == "c2" else f", time-boxed {budget:.0f} s"),
+                "seconds": round(time.perf_counter() - t_start, 1)}
+    import paper_1707_02423_b200 as P
+    best_d, best_i = best
+    nq, k = len(queries), len(mats)
+    allm = list(queries) + list(mats)
+    packed = pack(allm)
+    ia = rng.integers(0, nq, 4096)
+    ib = rng.integers(c0, c1, 4096)
+    with P.DeviceCorpus(queries) as Q, P.DeviceCorpus(mats) as Cc:
+        dg, _, itg, _ = P.isorank_pairs(Q, Cc, ia, ib, precision=args.precision)
+    d, _, it, _ = ffi.iso_batch(packed, ia.astype(np.int32), (nq + ib).astype(np.int32), threads=threads)
+    out = {"checked": "4096 random (query, corpus) pairs via isorank_pairs + best matches of sampled queries, "
+                      "vs oracle/isorank_ref.c", "pairs": 4096, "iter_mismatches": int((itg != it).sum()),
+           "max_rel_err": float(np.max(np.abs(dg - d) / d)),
+           "tolerance": 1e-9 if args.precision == "fp64" else 1e-5}
+    qs, best_ok = 0, 0
+    for q in rng.permutation(nq):
+        if time.perf_counter() - t_start > budget and qs > 0:
+            break
+        ib2 = np.arange(c0, c1)
+        dq, *_ = ffi.iso_batch(packed, np.full(len(ib2), q, np.int32), (nq + ib2).astype(np.int32), threads=threads)
+        j = int(np.argmin(dq))
+        best_ok += int(int(best_i[q]) == c0 + j and abs(float(best_d[q]) - dq[j]) <= 1e-9 * dq[j])
+        qs += 1
+    out.update({"best_match_queries": qs, "best_match_equal": best_ok,
+                "seconds": round(time.perf_counter() - t_start, 1)})
+    return out
 
 
 def two_product_flops(mats_a, mats_b, ia, ib, iters, sample=4000, seed=7):
@@ -403,6 +547,16 @@ def run_ours(args):
         tp_flops, sampled = two_product_flops(mats, mats, ga, gb, iters_local)
         work_note = "exact iteration counts of every unit" + ("; F sampled" if sampled else "")
 
+    # ---- parity of what this step produced (the checker; outside the timed region)
+    parity = None
+    if not args.no_parity and rank == 0:  # rank 0's own units / shard
+        if args.config == "c3":
+            parity = parity_check(args, mats, queries, best=(best_d.cpu().numpy(), best_i.cpu().numpy()),
+                                  c0=c0, c1=c1)
+        else:
+            parity = parity_check(args, mats, None, d_units=d_lin[: u1 - u0].cpu().numpy(), it_units=iters_local,
+                                  ga=ga, gb=gb)
+
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
@@ -508,7 +662,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, thr, n, t = cpu_sample(mats, args.cpu_seconds, queries=queries)
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{n} random pairs of this workload, {t:.1f} s wall on {thr} threads; "
                          "C restatement of sasscfg isorank (oracle/isorank_ref.c)"}
 
@@ -533,7 +687,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic (seeded CFG corpus following the reference's listing/edge-weighting rules)",
-            "config": dict(workload_desc(cfg, args, k), launch=graph_note),
+            "config": workload_desc(cfg, args, k), "launch": graph_note,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": src,
                          "work": "executed rank-K product 2 N^2 (K+1) flops per alignment (X_K = U C V^T, "
@@ -543,7 +697,8 @@ def run_ours(args):
                              "achieved": achieved_tp, "frac": achieved_tp / peak, "flops_per_step": tp_all,
                              "note": "SURVEY 8(d) F = sum_iters [2N(S_A+S_B) + N(z_A+z_B) + 8N^2]: the reference "
                                      "iteration's work; the closed form executes far less, so this exceeds 1"}},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
             "step_ms": [round(x, 3) for x in step_ms],
         }
         print(json.dumps(line), flush=True)

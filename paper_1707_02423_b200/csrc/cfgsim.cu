@@ -76,8 +76,29 @@ struct DBuf {
   }
 };
 
+// Pinned host buffer, grow-only (staging of host outputs and corpus uploads).
+struct PinBuf {
+  void *p = nullptr;
+  size_t n = 0;
+  ~PinBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t grow(size_t bytes) {
+    if (n >= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+};
+
 }  // namespace
 
+// A packed corpus in one device allocation: CSR, CSC, graph sizes, the
+// size-sorted permutation and the triangle row starts, uploaded with one
+// copy from pinned staging (include/cfgsim.h "Packed corpus").
 struct cfgsim_corpus {
   int device = 0;
   int32_t K = 0;
@@ -86,21 +107,25 @@ struct cfgsim_corpus {
   std::vector<int32_t> perm;      // sorted position -> graph (n desc, index asc)
   std::vector<int32_t> n_sorted;  // n of perm[a]
   std::vector<int64_t> row_start; // triangle units: K+1
-  DBuf d_n, d_rp_off, d_rowptr, d_nz_off, d_col, d_val, d_perm, d_row_start;
-  DBuf d_cscp, d_csc_row, d_csc_val;  // transposed copy (large-N kernel)
+  DBuf d_all;                     // every device array below lives in here
+  const int32_t *d_n = nullptr, *d_rowptr = nullptr, *d_col = nullptr, *d_perm = nullptr;
+  const int64_t *d_rp_off = nullptr, *d_nz_off = nullptr, *d_row_start = nullptr;
+  const double *d_val = nullptr;
+  const int32_t *d_cscp = nullptr, *d_csc_row = nullptr;  // transposed copy (large-N kernel)
+  const double *d_csc_val = nullptr;
   int64_t bytes = 0;
   DevCorpus dev() const {
     DevCorpus c;
     c.n_graphs = K;
-    c.n_nodes = d_n.as<int32_t>();
-    c.rp_off = d_rp_off.as<int64_t>();
-    c.rowptr = d_rowptr.as<int32_t>();
-    c.nz_off = d_nz_off.as<int64_t>();
-    c.col = d_col.as<int32_t>();
-    c.val = d_val.as<double>();
-    c.cscp = d_cscp.as<int32_t>();
-    c.csc_row = d_csc_row.as<int32_t>();
-    c.csc_val = d_csc_val.as<double>();
+    c.n_nodes = d_n;
+    c.rp_off = d_rp_off;
+    c.rowptr = d_rowptr;
+    c.nz_off = d_nz_off;
+    c.col = d_col;
+    c.val = d_val;
+    c.cscp = d_cscp;
+    c.csc_row = d_csc_row;
+    c.csc_val = d_csc_val;
     return c;
   }
 };
@@ -220,6 +245,8 @@ struct Scratch {
   DBuf seq_u, seq_d, seq_g, seq_n, seq_off, seq_st, seq_list, seq_apow;  // two-stage combos
   std::string seq_key;  // identity of the combo tables currently uploaded ("" = none)
   int64_t ovf_cap = 0;
+  DBuf pool_lin, pool_it, pool_out[4];  // per-call outputs, grow-only (no cudaMalloc/cudaFree per call)
+  PinBuf pin_out[4], pin_in;            // pinned staging of host outputs / corpus uploads
   std::recursive_mutex mu;
   cudaEvent_t done = nullptr;  // recorded at the end of the last call's stream work
   int depth = 0;               // nesting of guards on the owning thread
@@ -723,8 +750,8 @@ int seq_allpairs_t(const cfgsim_corpus *c, int64_t us, int64_t ue, const cfgsim_
     w.n_items = gu1 - gu0;
     w.u0 = gu0;
     w.out_base = out_base;
-    w.row_start = c->d_row_start.as<int64_t>();
-    w.perm = c->d_perm.as<int32_t>();
+    w.row_start = c->d_row_start;
+    w.perm = c->d_perm;
     w.K = c->K;
     PairOut o{};
     o.d = d_lin;
@@ -823,14 +850,37 @@ int set_device(int dev) {
   return CFGSIM_OK;
 }
 
-// Output staging: device pointers are used in place, host pointers staged.
+// Host copy of a large buffer on several threads (pinned staging -> user memory).
+void parallel_memcpy(void *dst, const void *src, size_t n) {
+  const size_t kChunk = 4u << 20;
+  const int nt = (int)std::min<size_t>(std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency())),
+                                       (n + kChunk - 1) / kChunk);
+  if (nt <= 1) {
+    memcpy(dst, src, n);
+    return;
+  }
+  const size_t per = (n + nt - 1) / nt;
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; t++) {
+    const size_t a = per * t, b = std::min(n, a + per);
+    if (a < b) pool.emplace_back([=] { memcpy((char *)dst + a, (const char *)src + a, b - a); });
+  }
+  memcpy(dst, src, std::min(n, per));
+  for (auto &th : pool) th.join();
+}
+
+// Output staging: device pointers are used in place; host pointers get a
+// device buffer (pooled in the device's Scratch when the caller passes one)
+// and, from 1 MB up, a pinned host buffer the D2H copy lands in (then one
+// multi-threaded memcpy into the caller's memory after the stream sync).
 struct OutStage {
-  void *user;
-  size_t bytes;
-  DBuf buf;
+  void *user = nullptr;
+  size_t bytes = 0;
+  DBuf own;
   void *dev = nullptr;
   bool host = false;
-  cudaError_t prepare(void *u, size_t b) {
+  PinBuf *pin = nullptr;
+  cudaError_t prepare(void *u, size_t b, cudaStream_t st = 0, DBuf *pool = nullptr, PinBuf *pinb = nullptr) {
     user = u;
     bytes = b;
     if (!u) return cudaSuccess;
@@ -839,13 +889,26 @@ struct OutStage {
       return cudaSuccess;
     }
     host = true;
-    cudaError_t e = buf.alloc(b);
-    dev = buf.p;
+    cudaError_t e;
+    if (pool) {
+      e = grow_buf(*pool, std::max<size_t>(b, 16), st);
+      dev = pool->p;
+    } else {
+      e = own.alloc(b);
+      dev = own.p;
+    }
+    if (e == cudaSuccess && pinb && b >= (1u << 20)) {
+      e = pinb->grow(b);  // (the previous user of this buffer synchronised before returning)
+      if (e == cudaSuccess) pin = pinb;
+    }
     return e;
   }
   cudaError_t finish(cudaStream_t st) {
-    if (user && host) return cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, st);
+    if (user && host) return cudaMemcpyAsync(pin ? pin->p : user, dev, bytes, cudaMemcpyDeviceToHost, st);
     return cudaSuccess;
+  }
+  void complete() {  // after the stream synchronised
+    if (user && host && pin) parallel_memcpy(user, pin->p, bytes);
   }
 };
 
@@ -1243,43 +1306,67 @@ int corpus_create_impl(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
   c->row_start[0] = 0;
   for (int a = 0; a < n_graphs; a++) c->row_start[a + 1] = c->row_start[a] + (n_graphs - a);
 
-  auto up = [&](DBuf &b, const void *src, size_t bytes) -> cudaError_t {
-    cudaError_t e = b.alloc(std::max<size_t>(bytes, 16));
-    if (e != cudaSuccess) return e;
-    c->bytes += (int64_t)bytes;
-    return bytes ? cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
-  };
-  cudaError_t e = cudaSuccess;
-  if (e == cudaSuccess) e = up(c->d_n, n_nodes, sizeof(int32_t) * n_graphs);
-  if (e == cudaSuccess) e = up(c->d_rp_off, rp_off, sizeof(int64_t) * n_graphs);
-  if (e == cudaSuccess) e = up(c->d_rowptr, rowptr, sizeof(int32_t) * rp_total);
-  if (e == cudaSuccess) e = up(c->d_nz_off, nz_off, sizeof(int64_t) * n_graphs);
-  if (e == cudaSuccess) e = up(c->d_col, col, sizeof(int32_t) * nz_total);
-  if (e == cudaSuccess) e = up(c->d_val, val, sizeof(double) * nz_total);
-  if (cscp_in) {  // prebuilt by the dense packer
-    if (e == cudaSuccess) e = up(c->d_cscp, cscp_in, sizeof(int32_t) * rp_total);
-    if (e == cudaSuccess) e = up(c->d_csc_row, crow_in, sizeof(int32_t) * nz_total);
-    if (e == cudaSuccess) e = up(c->d_csc_val, cval_in, sizeof(double) * nz_total);
-  } else {
-    std::vector<int32_t> cscp(rp_total, 0), crow(nz_total, 0);
-    std::vector<double> cval(nz_total, 0.0);
+  // host-side CSC unless the dense packer built it
+  std::vector<int32_t> cscp_v, crow_v;
+  std::vector<double> cval_v;
+  if (!cscp_in) {
+    cscp_v.assign(rp_total, 0);
+    crow_v.assign(nz_total, 0);
+    cval_v.assign(nz_total, 0.0);
     int bad = -1;
-    if (!build_csc(n_graphs, n_nodes, rp_off, rowptr, nz_off, col, val, cscp.data(), crow.data(), cval.data(),
+    if (!build_csc(n_graphs, n_nodes, rp_off, rowptr, nz_off, col, val, cscp_v.data(), crow_v.data(), cval_v.data(),
                    bad)) {
       delete c;
       return fail(CFGSIM_ERR_ARG, "column index out of range in graph " + std::to_string(bad));
     }
-    if (e == cudaSuccess) e = up(c->d_cscp, cscp.data(), sizeof(int32_t) * rp_total);
-    if (e == cudaSuccess) e = up(c->d_csc_row, crow.data(), sizeof(int32_t) * nz_total);
-    if (e == cudaSuccess) e = up(c->d_csc_val, cval.data(), sizeof(double) * nz_total);
+    cscp_in = cscp_v.data();
+    crow_in = crow_v.data();
+    cval_in = cval_v.data();
   }
-  if (e == cudaSuccess) e = up(c->d_perm, c->perm.data(), sizeof(int32_t) * n_graphs);
-  if (e == cudaSuccess) e = up(c->d_row_start, c->row_start.data(), sizeof(int64_t) * (n_graphs + 1));
+  // one allocation, 256-byte aligned sub-arrays, one H2D copy from pinned staging
+  struct Part { const void *src; size_t bytes; size_t at; };
+  std::vector<Part> parts = {
+      {n_nodes, sizeof(int32_t) * n_graphs, 0},          {rp_off, sizeof(int64_t) * n_graphs, 0},
+      {rowptr, sizeof(int32_t) * rp_total, 0},           {nz_off, sizeof(int64_t) * n_graphs, 0},
+      {col, sizeof(int32_t) * nz_total, 0},              {val, sizeof(double) * nz_total, 0},
+      {cscp_in, sizeof(int32_t) * rp_total, 0},          {crow_in, sizeof(int32_t) * nz_total, 0},
+      {cval_in, sizeof(double) * nz_total, 0},           {c->perm.data(), sizeof(int32_t) * n_graphs, 0},
+      {c->row_start.data(), sizeof(int64_t) * (n_graphs + 1), 0}};
+  size_t total = 0;
+  for (Part &pt : parts) {
+    pt.at = total;
+    total += (pt.bytes + 255) & ~size_t(255);
+  }
+  cudaError_t e = c->d_all.alloc(std::max<size_t>(total, 256));
+  if (e == cudaSuccess) {
+    Scratch &S = scratch_for(device);
+    std::lock_guard<std::recursive_mutex> lk(S.mu);
+    e = S.pin_in.grow(total);
+    if (e == cudaSuccess) {
+      unsigned char *h = (unsigned char *)S.pin_in.p;
+      for (const Part &pt : parts)
+        if (pt.bytes) memcpy(h + pt.at, pt.src, pt.bytes);
+      e = cudaMemcpy(c->d_all.p, h, total, cudaMemcpyHostToDevice);
+    }
+  }
   if (e != cudaSuccess) {
     delete c;
     return fail(e == cudaErrorMemoryAllocation ? CFGSIM_ERR_NOMEM : CFGSIM_ERR_CUDA,
                 std::string("corpus upload: ") + cudaGetErrorString(e));
   }
+  unsigned char *base = (unsigned char *)c->d_all.p;
+  c->d_n = (const int32_t *)(base + parts[0].at);
+  c->d_rp_off = (const int64_t *)(base + parts[1].at);
+  c->d_rowptr = (const int32_t *)(base + parts[2].at);
+  c->d_nz_off = (const int64_t *)(base + parts[3].at);
+  c->d_col = (const int32_t *)(base + parts[4].at);
+  c->d_val = (const double *)(base + parts[5].at);
+  c->d_cscp = (const int32_t *)(base + parts[6].at);
+  c->d_csc_row = (const int32_t *)(base + parts[7].at);
+  c->d_csc_val = (const double *)(base + parts[8].at);
+  c->d_perm = (const int32_t *)(base + parts[9].at);
+  c->d_row_start = (const int64_t *)(base + parts[10].at);
+  for (const Part &pt : parts) c->bytes += (int64_t)pt.bytes;
   *out = c;
   return CFGSIM_OK;
 }
@@ -1404,11 +1491,12 @@ int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t
       return fail(CFGSIM_ERR_ARG, "pair index out of range");
   std::vector<int64_t> slot(n_pairs);
   std::iota(slot.begin(), slot.end(), 0);
+  Scratch &S = scratch_for(A->device);
   OutStage sd, sw, si, sc;
-  CU(sd.prepare(d, sizeof(double) * n_pairs));
-  CU(sw.prepare(W, sizeof(double) * n_pairs));
-  CU(si.prepare(iters, sizeof(int32_t) * n_pairs));
-  CU(sc.prepare(converged, sizeof(uint8_t) * n_pairs));
+  CU(sd.prepare(d, sizeof(double) * n_pairs, st, &S.pool_out[0], &S.pin_out[0]));
+  CU(sw.prepare(W, sizeof(double) * n_pairs, st, &S.pool_out[1], &S.pin_out[1]));
+  CU(si.prepare(iters, sizeof(int32_t) * n_pairs, st, &S.pool_out[2], &S.pin_out[2]));
+  CU(sc.prepare(converged, sizeof(uint8_t) * n_pairs, st, &S.pool_out[3], &S.pin_out[3]));
   if (int rc = run_list(A, B, ha, hb, slot, p, (double *)sd.dev, (double *)sw.dev,
                         (int32_t *)si.dev, (uint8_t *)sc.dev, nullptr, nullptr, nullptr, st))
     return rc;
@@ -1418,6 +1506,10 @@ int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t
   CU(si.finish(st));
   CU(sc.finish(st));
   CU(cudaStreamSynchronize(st));
+  sd.complete();
+  sw.complete();
+  si.complete();
+  sc.complete();
   return CFGSIM_OK;
 }
 
@@ -1472,8 +1564,8 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   w.mode = WORK_TRIANGLE;
   w.ordered = ordered;
   w.out_base = u0;
-  w.row_start = c->d_row_start.as<int64_t>();
-  w.perm = c->d_perm.as<int32_t>();
+  w.row_start = c->d_row_start;
+  w.perm = c->d_perm;
   w.K = c->K;
   PairOut o{};
   o.d = d_lin;
@@ -1549,8 +1641,8 @@ int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const doubl
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int64_t nu = c->row_start[c->K];
   g_launches++;
-  scatter_kernel<<<1184, 256, 0, st>>>(nu, c->K, c->d_row_start.as<int64_t>(),
-                                       c->d_perm.as<int32_t>(), ordered, d_lin, iters_lin, d_mat,
+  scatter_kernel<<<1184, 256, 0, st>>>(nu, c->K, c->d_row_start,
+                                       c->d_perm, ordered, d_lin, iters_lin, d_mat,
                                        iters_mat);
   CU(cudaGetLastError());
   return CFGSIM_OK;
@@ -1565,21 +1657,22 @@ int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params
   DeviceGuard guard(c->device, st);
   const int64_t nu = c->row_start[c->K];
   const int64_t slots = ordered ? 2 * nu : nu;
-  DBuf dl, il;
-  CU(dl.alloc(sizeof(double) * slots));
-  if (iters_mat) CU(il.alloc(sizeof(int32_t) * slots));
-  if (int rc = cfgsim_allpairs_range(c, 0, nu, ordered, p, dl.as<double>(), il.as<int32_t>(), st))
-    return rc;
+  Scratch &S = scratch_for(c->device);
+  CU(grow_buf(S.pool_lin, sizeof(double) * slots, st));
+  if (iters_mat) CU(grow_buf(S.pool_it, sizeof(int32_t) * slots, st));
+  double *dl = S.pool_lin.as<double>();
+  int32_t *il = iters_mat ? S.pool_it.as<int32_t>() : nullptr;
   const size_t KK = (size_t)c->K * c->K;
   OutStage sd, si;
-  CU(sd.prepare(d_mat, sizeof(double) * KK));
-  CU(si.prepare(iters_mat, sizeof(int32_t) * KK));
-  if (int rc = cfgsim_allpairs_scatter(c, ordered, dl.as<double>(), il.as<int32_t>(),
-                                       (double *)sd.dev, (int32_t *)si.dev, st))
-    return rc;
+  CU(sd.prepare(d_mat, sizeof(double) * KK, st, &S.pool_out[0], &S.pin_out[0]));
+  CU(si.prepare(iters_mat, sizeof(int32_t) * KK, st, &S.pool_out[1], &S.pin_out[1]));
+  if (int rc = cfgsim_allpairs_range(c, 0, nu, ordered, p, dl, il, st)) return rc;
+  if (int rc = cfgsim_allpairs_scatter(c, ordered, dl, il, (double *)sd.dev, (int32_t *)si.dev, st)) return rc;
   CU(sd.finish(st));
   CU(si.finish(st));
   CU(cudaStreamSynchronize(st));
+  sd.complete();
+  si.complete();
   return CFGSIM_OK;
 }
 
@@ -1645,10 +1738,10 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
   cudaStream_t st = (cudaStream_t)cuda_stream;
   DeviceGuard guard(Q->device, st);
   const int32_t nq = Q->K, nc = c1 - c0;
-  OutStage sd, si;
-  CU(sd.prepare(best_d, sizeof(double) * nq));
-  CU(si.prepare(best_idx, sizeof(int64_t) * nq));
   Scratch &S = scratch_for(Q->device);
+  OutStage sd, si;
+  CU(sd.prepare(best_d, sizeof(double) * nq, st, &S.pool_out[0], &S.pin_out[0]));
+  CU(si.prepare(best_idx, sizeof(int64_t) * nq, st, &S.pool_out[1], &S.pin_out[1]));
   if (int rc = ensure_scratch(S, 1 << 16)) return rc;
   // corpus range in ascending node count (stable): pairs are enumerated as
   // rectangles of equal N = max(n_q, n_c) (two per distinct N) in these orders
@@ -1660,8 +1753,9 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
   CU(cudaMemcpyAsync(dcs.p, cs.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, st));
   // query blocks: one block's distance matrix stays <= 2^28 entries (2 GiB)
   const int64_t per_block = std::max<int64_t>(1, ((int64_t)1 << 28) / nc);
-  DBuf dm, dqs;
-  CU(dm.alloc(sizeof(double) * std::min<int64_t>(nq, per_block) * nc));
+  DBuf dqs;
+  CU(grow_buf(S.pool_lin, sizeof(double) * std::min<int64_t>(nq, per_block) * nc, st));  // the distance block
+  double *const dmp = S.pool_lin.as<double>();
   CU(dqs.alloc(sizeof(int32_t) * std::min<int64_t>(nq, per_block)));
   const bool lr = use_lowrank();
   for (int32_t q0 = 0; q0 < nq; q0 += (int32_t)per_block) {
@@ -1699,9 +1793,9 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
         if (N <= kSeqNmax) small.push_back(N);
       const int rc = p->precision == CFGSIM_FP32
                          ? seq_nearest_t<float>(Q, C, qs, cs, dqs.as<int32_t>(), dcs.as<int32_t>(), q0, c0, nc, small,
-                                                p, dm.as<double>(), launch_no2, st)
+                                                p, dmp, launch_no2, st)
                          : seq_nearest_t<double>(Q, C, qs, cs, dqs.as<int32_t>(), dcs.as<int32_t>(), q0, c0, nc, small,
-                                                 p, dm.as<double>(), launch_no2, st);
+                                                 p, dmp, launch_no2, st);
       if (rc) return rc;
     }
     for (int N : ns) {
@@ -1740,7 +1834,7 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
       w.cbase = c0;
       w.ld = nc;
       PairOut o{};
-      o.d = dm.as<double>();
+      o.d = dmp;
       o.ovf_count = S.ovf_count.as<int32_t>();
       o.ovf_list = S.ovf_list.as<int64_t>();
       o.ovf_cap = (int32_t)S.ovf_cap;
@@ -1780,18 +1874,20 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
           rsl[kind].push_back((int64_t)(gq - q0) * nc + (gc - c0));
         }
         for (int kind = 0; kind < 2; kind++)
-          if (int rc = run_list(Q, C, ra[kind], rb[kind], rsl[kind], p, dm.as<double>(), nullptr, nullptr, nullptr,
+          if (int rc = run_list(Q, C, ra[kind], rb[kind], rsl[kind], p, dmp, nullptr, nullptr, nullptr,
                                 nullptr, nullptr, nullptr, st, kind == 0 ? 1 : 2))
             return rc;
       }
     }
     if (int rc = big_status(S, st)) return rc;
-    rowmin_kernel<<<bq, 256, 0, st>>>(bq, nc, dm.as<double>(), c0, (double *)sd.dev + q0, (int64_t *)si.dev + q0);
+    rowmin_kernel<<<bq, 256, 0, st>>>(bq, nc, dmp, c0, (double *)sd.dev + q0, (int64_t *)si.dev + q0);
     CU(cudaGetLastError());
   }
   CU(sd.finish(st));
   CU(si.finish(st));
   CU(cudaStreamSynchronize(st));
+  sd.complete();
+  si.complete();
   return CFGSIM_OK;
 }
 

@@ -42,9 +42,28 @@ def test_interpolate_bit_exact(P):
 
 
 # ------------------------------------------------------------ single pairs
+def greedy_is_untied(X, rel=1e-9):
+    """True when every round of _greedy_matching (similarity.py:96-108) on X
+    has a unique best entry by a margin (then any correct implementation must
+    return the reference's own matching)."""
+    w = np.array(X, float)
+    for _ in range(w.shape[0]):
+        flat = w.ravel()
+        top = np.partition(flat, -2)[-2:] if flat.size > 1 else np.array([-1.0, flat[0]])
+        best, second = float(top.max()), float(top.min())
+        if flat.size > 1 and best - second <= rel * max(abs(best), 1e-300):
+            return False
+        r, c = divmod(int(np.argmax(flat)), w.shape[1])
+        w[r, :] = -1.0
+        w[:, c] = -1.0
+    return True
+
+
 def test_small_pairs_against_reference(P):
     g = load_golden("small_pairs.npz")
     A, B, X = unravel(g["sa"], g["fa"]), unravel(g["sb"], g["fb"]), unravel(g["sx"], g["fx"])
+    offs = np.concatenate([[0], np.cumsum(g["sx"])])
+    untied = 0
     for i, (a, b) in enumerate(zip(A, B)):
         d = P.measure_distance(mat(P, a), mat(P, b), P.MeasureId.ISO)
         assert d == pytest.approx(g["d"][i], rel=1e-12, abs=1e-12), i
@@ -55,6 +74,10 @@ def test_small_pairs_against_reference(P):
             np.testing.assert_allclose(al.matrix, X[i], rtol=1e-10, atol=1e-15)
             assert al.matched_weight == pytest.approx(g["W"][i], rel=1e-12)
             assert sorted(al.matching) == list(range(a.shape[0]))
+            if greedy_is_untied(X[i]):  # the reference's own permutation
+                assert al.matching == tuple(int(v) for v in g["match"][offs[i]:offs[i + 1]]), i
+                untied += 1
+    assert untied >= 20
 
 
 def test_reference_pinned_cases(P):
