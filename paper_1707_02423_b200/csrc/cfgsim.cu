@@ -699,10 +699,33 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
   const T *useq = S.seq_u.as<T>();
   const double *dseq = S.seq_d.as<double>();
   const int64_t *uo = S.seq_off.as<int64_t>();
+  static const bool phases = [] {
+    const char *e = getenv("CFGSIM_PHASES");
+    return e && atoi(e) != 0;
+  }();
+  static DBuf phase_buf;
+  pp.phase = nullptr;
+  if (phases) {
+    if (!phase_buf.p) CU(phase_buf.alloc(16 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(phase_buf.p, 0, 16 * sizeof(unsigned long long), st));
+    pp.phase = phase_buf.as<unsigned long long>();
+  }
   void *args[] = {(void *)&nn, (void *)&w, (void *)&o, (void *)&pp, (void *)&useq, (void *)&dseq, (void *)&uo,
                   (void *)&ctr};
   CU(cudaLaunchKernel(f2, dim3((unsigned)grid), dim3(nt), args, smem, st));
   g_launches++;
+  if (pp.phase) {
+    unsigned long long ph[16];
+    CU(cudaMemcpyAsync(ph, pp.phase, sizeof(ph), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    double tp = 0, tc = 0;
+    for (int k = 0; k < 5; k++) tp += (double)ph[k];
+    for (int k = 8; k < 10; k++) tc += (double)ph[k];
+    fprintf(stderr, "[cfgsim pair2 N=%d items=%lld grid=%lld] producer: wait/claim %.1f%% bracket+delta %.1f%% "
+            "stage+mma+keys %.1f%% row-orders %.1f%% tail %.1f%% (%.3e cyc) | consumer: wait %.1f%% rounds %.1f%% "
+            "(%.3e cyc)\n", N, (long long)w.n_items, (long long)grid, 100 * ph[0] / tp, 100 * ph[1] / tp,
+            100 * ph[2] / tp, 100 * ph[3] / tp, 100 * ph[4] / tp, tp, 100 * ph[8] / tc, 100 * ph[9] / tc, tc);
+  }
   return CFGSIM_OK;
 }
 

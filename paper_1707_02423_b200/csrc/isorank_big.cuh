@@ -116,7 +116,7 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
   s.vs = take(sizeof(T) * 2 * BIG_KC * BIG_VP);
   const size_t gemm_end = o;
   o = base;
-  s.taken = take(sizeof(uint32_t) * 32);
+  s.taken = take(sizeof(uint32_t) * 64);  // two generations (race-free update)
   s.gslot = take(sizeof(unsigned long long) * 2 * BIG_WARPS + sizeof(int32_t) * (4 * BIG_WARPS + 2));
   s.mrow = take(sizeof(int32_t) * nlim);
   s.mval = take(sizeof(unsigned long long) * nlim);
@@ -818,7 +818,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         int32_t *slot_c = slot_r + 2 * BIG_WARPS;
         int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
         unsigned long long *mval = (unsigned long long *)(smem_raw + L.mval);
-        for (int w = tid; w < 32; w += NT) taken[w] = 0u;
+        for (int w = tid; w < 64; w += NT) taken[w] = 0u;
         constexpr int PF = 3;  // prefetch depth (positions ahead of the head)
         unsigned long long hv[BIG_R], qv[BIG_R][PF];
         int hc[BIG_R], qc[BIG_R][PF], ptr[BIG_R];
@@ -845,6 +845,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         }
         __syncthreads();
         if (prm.phase && tid == 0) atomicAdd(prm.phase + 7, (unsigned long long)N);
+        int prev_col = 0;
         for (int round = 0; round < N; round++) {
           unsigned long long bv = 0ull;
           int brow = 0x7fffffff, bcl = 0;
@@ -883,7 +884,16 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
               bcol = slot_c[buf * BIG_WARPS + w];
             }
           }
-          taken[bcol >> 5] |= 1u << (bcol & 31);  // every thread writes the same bit
+          // taken columns, two generations: round r reads T_r from buffer r & 1
+          // (plus this round's column, in registers); thread 0 writes T_{r+1}
+          // into the other buffer, whose last readers were in round r - 1
+          const uint32_t *tk_cur = taken + (round & 1) * 32;
+          if (tid == 0) {
+            uint32_t *tk_nxt = taken + ((round + 1) & 1) * 32;
+            if (round > 0) tk_nxt[prev_col >> 5] |= 1u << (prev_col & 31);
+            tk_nxt[bcol >> 5] |= 1u << (bcol & 31);
+          }
+          prev_col = bcol;
           if ((grow & (BIG_THREADS - 1)) == tid) {
             act &= ~(1u << (grow / BIG_THREADS));
             mrow[grow] = bcol;
@@ -907,7 +917,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
                   qv[r][PF - 1] = sval[(size_t)i * N + p + PF];
                   qc[r][PF - 1] = scol[(size_t)i * N + p + PF];
                 }
-              } while ((taken[hc[r] >> 5] >> (hc[r] & 31)) & 1u);
+              } while (hc[r] == bcol || ((tk_cur[hc[r] >> 5] >> (hc[r] & 31)) & 1u));
               ptr[r] = p;
               if (prm.phase) {  // diagnostics: advances, advances past the prefetched window
                 atomicAdd(prm.phase + 5, (unsigned long long)steps);

@@ -330,7 +330,21 @@ struct Pair2Params {
   int64_t cbase;    // combo index = cbase + sorted position (triangle; rect: query side)
   int64_t cbase2;   // rect mode: combo index of the corpus side = cbase2 + sorted position
   const double *apow;  // alpha^m, m = 0..kcap, by sequential products (host)
+  unsigned long long *phase;  // optional (CFGSIM_PHASES=1): cycles per phase, summed over CTAs
 };
+
+// per-phase cycle accounting of the stage-2 kernel (debug; phase == nullptr
+// in production): slot k accumulates the cycles from mark k to the next mark
+// of the same role (producer warp 0 lane 0: slots 0-4; consumer lane 0: 8-9)
+#define P2_PHASE(k)                                                     \
+  do {                                                                  \
+    if (prm.phase && (tid == 0 || tid == NP)) {                         \
+      const unsigned long long now_ = clock64();                        \
+      if (ph_last >= 0) atomicAdd(prm.phase + ph_last, now_ - ph_t);    \
+      ph_t = now_;                                                      \
+      ph_last = (k);                                                    \
+    }                                                                   \
+  } while (0)
 
 // Stage-2 kernel, warp-specialised: warps 0..PW-1 ("producers") compute pair
 // p's stopping sweep, X_K and row orders into one of two shared-memory
@@ -762,11 +776,15 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     // ---------------- consumer: greedy rounds of the pairs in order
     // (a second consumer warp owning one buffer each measured 2% slower)
     int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
+    unsigned long long ph_t = 0;
+    int ph_last = -1;
     for (int it = 0;; it++) {
       const int s = it & 1;
+      P2_PHASE(8);  // wait for a full buffer
       nbar_sync(BAR_FULL + s, NALL);
+      P2_PHASE(9);  // greedy rounds + outputs
       const P2Meta mt = meta[s];
-      if (!mt.valid) break;
+      if (!mt.valid) { P2_PHASE(15); break; }
       const T *Xs = (const T *)(smem_raw + L.x[s]);
       const double wsum =
           mt.keys ? p2_rounds_keys<T, KB>((const unsigned long long *)Xs, 32 * KB + 1, smem_raw + L.ord[s], N, mt.emin,
@@ -793,8 +811,11 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   nbar_sync(BAR_P, NP);
   const int NPt = seq_pitch<T>(N);                      // history row pitch
   const int SPD = ((2 * NPt + 7) / 16) * 16 + 8;        // staged row pitch (== 8 mod 16 doubles: 2-wavefront fragments)
+  unsigned long long ph_t = 0;
+  int ph_last = -1;
   for (int it = 0;; it++) {
     const int s = it & 1;
+    P2_PHASE(0);  // claim an item + wait for the free buffer
     if (tid == 0) {
       *s_item = (int64_t)atomicAdd(counter, 1ull);
       s_first[0] = 0x7fffffff;
@@ -853,6 +874,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     const T *UB = useq + uoff[cb];
     const double *DA = dseq + ca * (int64_t)(prm.kcap + 1);
     const double *DB = dseq + cb * (int64_t)(prm.kcap + 1);
+    P2_PHASE(1);  // bracket scan + exact deltas
 
     // ---- stopping sweep K (similarity.py:139-146): every sweep's bracket in
     // parallel (alpha^m from the host's table, the same sequential products),
@@ -907,6 +929,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     // ---- X_K = sum_{m<K} (c alpha^m) u_m v_m^T + (alpha^K/N^2) u_K v_K^T, the
     // u/v rows staged through shared memory in chunks of P2_KC sweeps
     // (16-byte cp.async; rows past K zero-filled up to the chunk's end)
+    P2_PHASE(2);  // staging + rank-K product + key build
     const int nch = (K + 1 + P2_KC - 1) / P2_KC;  // rows m = 0..K
     // staging assignment: copy q (16 bytes) of rows mm0, mm0 + sstep, ...
     constexpr int EPU = 16 / sizeof(T);  // elements per 16-byte copy
@@ -926,6 +949,10 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     };
     stage(0);
     int emn = 0x7fffffff, emx = -1;
+    int emin = 0;
+    bool keys = true;
+    constexpr int PK = 32 * KB + 1;
+    unsigned long long *Kr = (unsigned long long *)Xs;
     {
       // fp64 tensor cores: mma.m8n8k4 accumulates each 8x8 tile as the fma
       // chain over k in order (bitwise equal to the scalar chain, probed on
@@ -998,10 +1025,8 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
         atomicMax(s_first + 2, emx);
       }
       nbar_sync(BAR_P, NP);
-      const int emin = s_first[1];
-      const bool keys = p2_use_keys<T>(emin, s_first[2]);  // the same predicate as the readers below
-      constexpr int PK = 32 * KB + 1;
-      unsigned long long *Kr = (unsigned long long *)Xs;
+      emin = s_first[1];
+      keys = p2_use_keys<T>(emin, s_first[2]);  // the same predicate as the readers below
 #pragma unroll
       for (int x = 0; x < TR; x++)
 #pragma unroll
@@ -1016,10 +1041,9 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
           }
     }
     nbar_sync(BAR_P, NP);
-    const int emin = s_first[1];
-    const bool keys = p2_use_keys<T>(emin, s_first[2]);
-    constexpr int PK = 32 * KB + 1;
-    unsigned long long *Kr = (unsigned long long *)Xs;
+    P2_PHASE(3);  // row orders
+    // (emin / keys were read before this barrier: thread 0 rewrites s_first
+    // for the next pair as soon as it passes it)
     if (keys) {
       // ---- row orders: one thread per row, 32-bit prefix keys in registers
       if constexpr (KB == 2) {  // two adjacent lanes per row
@@ -1041,7 +1065,9 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       meta[s].emin = emin;
     }
     nbar_arrive(BAR_FULL + s, NALL);  // publishes X, ord, meta (bar.arrive orders prior smem writes)
+    P2_PHASE(4);
   }
+  P2_PHASE(15);
 }
 
 }  // namespace cfgsim
