@@ -513,7 +513,7 @@ int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, 
     double tot = 0;
     for (int k = 0; k < 5; k++) tot += (double)ph[k];
     fprintf(stderr, "[cfgsim big N<=%d] phase cycles (sum over CTAs): operators %.1f%% sweeps %.1f%% gemm %.1f%% "
-            "sort %.1f%% greedy %.1f%% total %.3e | rounds %llu advances %llu deep %llu\n", nlim, 100 * ph[0] / tot,
+            "sort %.1f%% greedy %.1f%% total %.3e | sum N %llu proposals %llu (unused %llu)\n", nlim, 100 * ph[0] / tot,
             100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot, tot, ph[7], ph[5], ph[6]);
   }
   return CFGSIM_OK;

@@ -77,14 +77,21 @@ __host__ __device__ inline BigSlab big_slab_layout(int nlim, int kcap) {
   return s;
 }
 
+// staged row: element e at e + (e >> 5) (one pad word per 32), so the sort's
+// lane-contiguous reads (lane l: elements l * KB ..) spread over the banks
+__host__ __device__ inline int big_row_pitch(int nlim) { return nlim + (nlim >> 5) + 1; }
+__device__ __forceinline__ int big_rpos(int e) { return e + (e >> 5); }
+
 // dynamic shared memory: a persistent head + a union of the phase regions
 struct BigSmem {
   // sweep region (per side s = 0 (A), 1 (B))
   size_t lo[2], fr[2], rinv[2], pst[2], zf[2], t[2], ring[2], scr;
   // gemm region
   size_t us, vs;
+  // sort region: one staged X row per warp
+  size_t rows;
   // greedy region
-  size_t taken, gslot, mrow, mval;
+  size_t hold, dfl, taken, gslot, mrow, mval;
   size_t red, misc, total;
 };
 
@@ -116,13 +123,19 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
   s.vs = take(sizeof(T) * 2 * BIG_KC * BIG_VP);
   const size_t gemm_end = o;
   o = base;
-  s.taken = take(sizeof(uint32_t) * 64);  // two generations (race-free update)
+  s.rows = take(sizeof(T) * BIG_WARPS * (size_t)big_row_pitch(nlim));
+  const size_t sort_end = o;
+  o = base;
+  s.hold = take(2 * sizeof(unsigned long long) * nlim);  // per column: (value bits, 0xffff - row)
+  s.dfl = take(sizeof(uint8_t) * nlim);                  // per row: displaced in this step
+  s.taken = take(sizeof(uint32_t) * 64);  // (CFGSIM_BIG_ROUNDS) two generations of taken columns
   s.gslot = take(sizeof(unsigned long long) * 2 * BIG_WARPS + sizeof(int32_t) * (4 * BIG_WARPS + 2));
   s.mrow = take(sizeof(int32_t) * nlim);
   s.mval = take(sizeof(unsigned long long) * nlim);
   const size_t greedy_end = o;
   size_t e = sweep_end > gemm_end ? sweep_end : gemm_end;
   e = e > greedy_end ? e : greedy_end;
+  e = e > sort_end ? e : sort_end;
   s.total = e;
   return s;
 }
@@ -279,6 +292,20 @@ __device__ __forceinline__ unsigned long long big_bits(T v) {
 
 __device__ __forceinline__ int big_key_col(unsigned long long k) {
   return (1 << BIG_CB) - 1 - (int)(k & ((1ull << BIG_CB) - 1));
+}
+
+// 16-byte compare-and-swap in shared memory (sm_90+): {lo, hi} at addr
+__device__ __forceinline__ void big_cas128(unsigned long long *addr, unsigned long long cmp_lo,
+                                           unsigned long long cmp_hi, unsigned long long new_lo,
+                                           unsigned long long new_hi, unsigned long long &old_lo,
+                                           unsigned long long &old_hi) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(addr);
+  asm volatile(
+      "{\n .reg .b128 d, b, c;\n mov.b128 b, {%2, %3};\n mov.b128 c, {%4, %5};\n"
+      " atom.shared.cas.b128 d, [%6], b, c;\n mov.b128 {%0, %1}, d;\n}\n"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "r"(a)
+      : "memory");
 }
 
 __device__ __forceinline__ void big_cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -720,6 +747,8 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       // order; equal 22-bit prefixes with different exact values (near-ties,
       // ~1e-6 relative) are repaired by odd-even transposition on the exact
       // keys.  Exactly tied values keep column order from the key's low bits.
+#ifdef CFGSIM_BIG_NOSTAGE
+#define BIG_RP(e) (e)
       for (int i = warp; i < N; i += BIG_WARPS) {
         const T *row = X + (size_t)i * N;
         int rmin = 0x7fffffff, rmax = -1;
@@ -746,6 +775,44 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           }
           key[c] = k;
         }
+#else
+#define BIG_RP(e) big_rpos(e)
+      T *rbuf = (T *)(smem_raw + L.rows) + (size_t)warp * big_row_pitch(prm.nlim);
+      for (int i = warp; i < N; i += BIG_WARPS) {
+        // row i staged in shared memory with one coalesced pass (the sort's
+        // key build, exact-value gathers and near-tie repair then read it
+        // there instead of re-reading the HBM slab lane-strided / at random)
+        const T *grow = X + (size_t)i * N;
+        const T *row = rbuf;
+        int rmin = 0x7fffffff, rmax = -1;
+#pragma unroll 8
+        for (int j = lane; j < N; j += 32) {
+          const T v = grow[j];
+          rbuf[big_rpos(j)] = v;
+          const int e = big_exponent(v);
+          rmin = min(rmin, e);
+          rmax = max(rmax, e);
+        }
+        __syncwarp();
+        rmin = __reduce_min_sync(0xffffffffu, rmin);
+        rmax = __reduce_max_sync(0xffffffffu, rmax);
+        constexpr int MB = sizeof(T) == 8 ? 52 : 23;
+        const int rshift = (32 - __clz(rmax - rmin)) + MB - 22;  // value bits above the 22 kept
+        uint32_t key[KB];
+#pragma unroll
+        for (int c = 0; c < KB; c++) {
+          const int j = lane * KB + c;
+          uint32_t k = 0u;  // padding sorts last (a real key's column field is >= 1024 - N >= 1 then)
+          if (j < N) {
+            const unsigned long long b = big_bits(row[big_rpos(j)]);
+            const unsigned long long v =
+                ((((b >> MB) & (sizeof(T) == 8 ? 0x7ffull : 0xffull)) - (unsigned long long)rmin) << MB) |
+                (b & ((1ull << MB) - 1));
+            k = ((uint32_t)(v >> rshift) << BIG_CB) | (uint32_t)((1 << BIG_CB) - 1 - j);
+          }
+          key[c] = k;
+        }
+#endif
         big_sort_desc<uint32_t, KB>(key, lane);
         // pair-wide 64-bit keys (exponent | mantissa truncated by `shift` bits |
         // column) in sorted order; odd-even transposition repairs inversions
@@ -756,7 +823,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         for (int c = 0; c < KB; c++) {
           const int pos = lane * KB + c;
           const int col = (1 << BIG_CB) - 1 - (int)(key[c] & ((1u << BIG_CB) - 1));
-          ek[c] = (pos < N) ? big_sort_key<T>(row[col], col, emin, shift) : 0ull;
+          ek[c] = (pos < N) ? big_sort_key<T>(row[BIG_RP(col)], col, emin, shift) : 0ull;
         }
         // `after(x, y)`: y must precede x — (value desc, column asc), exact:
         // equal truncated values are decided on X (keys' low bits only hold
@@ -764,7 +831,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         auto after = [&](unsigned long long x, unsigned long long y) {
           if ((x >> BIG_CB) != (y >> BIG_CB)) return (x >> BIG_CB) < (y >> BIG_CB);
           if (shift > 0) {
-            const T vx = row[big_key_col(x)], vy = row[big_key_col(y)];
+            const T vx = row[BIG_RP(big_key_col(x))], vy = row[BIG_RP(big_key_col(y))];
             if (vx != vy) return vx < vy;
           }
           return (x & ((1ull << BIG_CB) - 1)) < (y & ((1ull << BIG_CB) - 1));  // lower column first
@@ -794,14 +861,16 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           const int pos = lane * KB + c;
           if (pos < N) {
             const int col = big_key_col(ek[c]);
-            ov[pos] = big_bits(row[col]);  // exact value bits for the rounds
+            ov[pos] = big_bits(row[BIG_RP(col)]);  // exact value bits for the matching
             oc[pos] = (uint16_t)col;
           }
         }
+        __syncwarp();  // rbuf is restaged for the warp's next row
       }
       __syncthreads();
 
       BIG_PHASE(4);
+#ifdef CFGSIM_BIG_ROUNDS
       // ---- 4b. greedy matching rounds, similarity.py:96-108, whole CTA.
       // Thread t owns rows t + 256 r (r < BIG_R); each active row's head is
       // its best untaken column, compared across rows on exact value bits
@@ -926,6 +995,169 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
             }
           }
         }
+#else
+      // ---- 4b. greedy matching, similarity.py:96-108, whole CTA, as
+      // row-proposing deferred acceptance (Gale-Shapley).  With edges
+      // totally ordered by (value desc, row asc, column asc) — the order in
+      // which np.argmax's first occurrence takes them — the greedy matching
+      // is the unique stable matching of rows and columns ranking each other
+      // by that order, so GS returns exactly it, in any proposal order.
+      // Rows walk their sorted orders; column c keeps the best proposal in a
+      // 16-byte (exact value bits, 0xffff - row) slot updated by 128-bit CAS;
+      // a displaced row resumes after the column it lost.  No per-round
+      // argmax or barrier: each thread's rows propose independently (their
+      // next sorted entries prefetched in registers), and a step only hands
+      // the displaced rows back to their owners.
+      {
+        unsigned long long *hold = (unsigned long long *)(smem_raw + L.hold);
+        uint8_t *dfl = (uint8_t *)(smem_raw + L.dfl);
+        int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
+        unsigned long long *mval = (unsigned long long *)(smem_raw + L.mval);
+        for (int c = tid; c < N; c += NT) {
+          hold[2 * c] = 0ull;  // free: (0, 0) loses to every real entry (values > 0)
+          hold[2 * c + 1] = 0ull;
+          dfl[c] = 0;
+        }
+        constexpr int PF = 3;  // prefetch depth (positions ahead of the head)
+        unsigned long long hv[BIG_R], qv[BIG_R][PF];
+        int hc[BIG_R], qc[BIG_R][PF], ptr[BIG_R];
+        uint32_t fr = 0u;  // rows of this thread without a column
+#pragma unroll
+        for (int r = 0; r < BIG_R; r++) {
+          const int i = tid + BIG_THREADS * r;
+          hv[r] = 0ull;
+          hc[r] = 0;
+          ptr[r] = 0;
+#pragma unroll
+          for (int f = 0; f < PF; f++) { qv[r][f] = 0ull; qc[r][f] = 0; }
+          if (i < N) {
+            fr |= 1u << r;
+            hv[r] = sval[(size_t)i * N];
+            hc[r] = scol[(size_t)i * N];
+#pragma unroll
+            for (int f = 0; f < PF; f++)
+              if (1 + f < N) {
+                qv[r][f] = sval[(size_t)i * N + 1 + f];
+                qc[r][f] = scol[(size_t)i * N + 1 + f];
+              }
+          }
+        }
+        // next sorted entry of row r (its head moves one position)
+        auto advance = [&](int r) {
+          const int i = tid + BIG_THREADS * r;
+          const int p = ++ptr[r];
+          hv[r] = qv[r][0];
+          hc[r] = qc[r][0];
+#pragma unroll
+          for (int f = 0; f + 1 < PF; f++) { qv[r][f] = qv[r][f + 1]; qc[r][f] = qc[r][f + 1]; }
+          if (p + PF < N) {
+            qv[r][PF - 1] = sval[(size_t)i * N + p + PF];
+            qc[r][PF - 1] = scol[(size_t)i * N + p + PF];
+          }
+        };
+#ifdef CFGSIM_BIG_GS_STEP
+        __syncthreads();
+        unsigned long long props = 0ull;
+        for (int step = 0;; step++) {
+          while (fr) {
+#pragma unroll
+            for (int r = 0; r < BIG_R; r++) {
+              if ((fr >> r) & 1u) {
+                const int i = tid + BIG_THREADS * r;
+                const unsigned long long v = hv[r], rc = (unsigned long long)(0xffff - i);
+                unsigned long long *slot = hold + 2 * hc[r];
+                unsigned long long ev = 0ull, er = 0ull, ov, orr;
+                bool won;
+                ++props;
+                for (;;) {
+                  big_cas128(slot, ev, er, v, rc, ov, orr);
+                  if (ov == ev && orr == er) { won = true; break; }
+                  if (ov > v || (ov == v && orr > rc)) { won = false; break; }
+                  ev = ov;
+                  er = orr;
+                }
+                if (won) {
+                  fr &= ~(1u << r);
+                  mrow[i] = hc[r];
+                  mval[i] = v;
+                  if (ov) dfl[0xffff - (int)orr] = 1;
+                } else {
+                  advance(r);
+                }
+              }
+            }
+          }
+          __syncthreads();
+          int mine = 0;
+#pragma unroll
+          for (int r = 0; r < BIG_R; r++) {
+            const int i = tid + BIG_THREADS * r;
+            if (i < N && dfl[i]) {
+              dfl[i] = 0;
+              fr |= 1u << r;
+              advance(r);
+              mine = 1;
+            }
+          }
+          if (!__syncthreads_or(mine)) break;
+        }
+#else
+        int *nheld = (int *)(smem_raw + L.misc + 96);  // columns with a holder
+        if (tid == 0) *nheld = 0;
+        __syncthreads();
+        unsigned long long props = 0ull;
+        // fully asynchronous: a thread proposes for its free rows, takes back
+        // rows another thread displaced (flag dfl), and spins until every
+        // column has a holder (then every row holds one: N rows, N columns)
+        for (;;) {
+          bool did = false;
+#pragma unroll
+          for (int r = 0; r < BIG_R; r++) {
+            const int i = tid + BIG_THREADS * r;
+            if (i < N && ((volatile uint8_t *)dfl)[i]) {
+              dfl[i] = 0;
+              fr |= 1u << r;
+              advance(r);
+            }
+          }
+          while (fr) {
+            did = true;
+#pragma unroll
+            for (int r = 0; r < BIG_R; r++) {
+              if ((fr >> r) & 1u) {
+                const int i = tid + BIG_THREADS * r;
+                const unsigned long long v = hv[r], rc = (unsigned long long)(0xffff - i);
+                unsigned long long *slot = hold + 2 * hc[r];
+                unsigned long long ev = 0ull, er = 0ull, ov, orr;
+                bool won;
+                ++props;
+                for (;;) {
+                  big_cas128(slot, ev, er, v, rc, ov, orr);
+                  if (ov == ev && orr == er) { won = true; break; }
+                  if (ov > v || (ov == v && orr > rc)) { won = false; break; }
+                  ev = ov;
+                  er = orr;
+                }
+                if (won) {
+                  fr &= ~(1u << r);
+                  mrow[i] = hc[r];
+                  mval[i] = v;
+                  if (ov) ((volatile uint8_t *)dfl)[0xffff - (int)orr] = 1;  // the previous holder is free again
+                  else atomicAdd(nheld, 1);
+                } else {
+                  advance(r);
+                }
+              }
+            }
+          }
+          if (*(volatile int *)nheld >= N) break;
+          if (!did) __nanosleep(32);
+        }
+        __syncthreads();
+#endif
+        if (prm.phase) atomicAdd(prm.phase + 5, props);  // diagnostics: proposals
+        if (prm.phase && tid == 0) atomicAdd(prm.phase + 7, (unsigned long long)N);
+#endif
         __syncthreads();
         if (tid == 0) {  // similarity.py:150: Python sum in row order
           double wsum = 0.0;

@@ -366,8 +366,35 @@ struct P2Meta {
 };
 
 struct P2Smem {
-  size_t x[2], ord[2], meta, red, amb, item, first, mrow, tab, total;
+  size_t x[2], ord[2], meta, red, amb, item, first, tab, total;
 };
+
+// staged history row pitch (elements; holds u_m and v_m side by side, >= 2
+// NPt) such that the mma fragment loads (lane = 4 lr + lk reads row lk,
+// column lr) are conflict-free: fp64 — a 64-bit request is served per
+// half-warp, and 2 pitch mod 32 banks must be 8 or 24 so that the four rows
+// lk land in disjoint bank octets (pitch == 4 mod 16; pitch == 8 mod 16 put
+// rows 0 and 2 on the same banks: 2-way conflicts, measured);  fp32 — rows
+// at pitch == 8 mod 16 floats start on bank octets 0/8/16/24.
+__host__ __device__ inline int p2_stage_pitch(int npt, int tsize) {
+#ifdef CFGSIM_SPD_OLD
+  return ((2 * npt + 7) / 16) * 16 + 8;
+#else
+  return tsize == 8 ? ((2 * npt + 11) / 16) * 16 + 4 : ((2 * npt + 7) / 16) * 16 + 8;
+#endif
+}
+
+// row-order pitch in bytes: an odd number of 4-byte words, so the rows a
+// warp touches at one position (one row per lane) fall in distinct banks
+// (pitch N put 16-32 rows in one bank: 8-16-way conflicts on every order
+// write and on the consumer's head reads)
+__host__ __device__ inline int p2_ord_pitch(int N) {
+#ifdef CFGSIM_ORD_NOPAD
+  return N;
+#else
+  return 4 * (((N + 3) / 4) | 1);
+#endif
+}
 
 __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
   P2Smem s;
@@ -377,20 +404,19 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
     o += (b + 15) & ~size_t(15);
     return at;
   };
-  const int npt = (N + 3) & ~3, spd = ((2 * npt + 7) / 16) * 16 + 8;  // >= either T's pitch
+  const int npt = (N + 3) & ~3, spd = p2_stage_pitch(npt, 8) > p2_stage_pitch(npt, 4) ? p2_stage_pitch(npt, 8) : p2_stage_pitch(npt, 4);  // >= either T's pitch
   size_t xb = (size_t)tsize * N * (N | 1), sb = (size_t)8 * 2 * P2_KC * spd;
   const size_t kb = 8 * (size_t)N * (N <= 32 ? 33 : 65);  // key rows (pitch 32 KB + 1)
   if (kb > xb) xb = kb;
   for (int q = 0; q < 2; q++) {
     s.x[q] = take(xb > sb ? xb : sb);  // X_K (aliases the u/v staging while it is built)
-    s.ord[q] = take((size_t)N * N);    // row orders (columns, value desc / column asc)
+    s.ord[q] = take((size_t)N * p2_ord_pitch(N));  // row orders (columns, value desc / column asc)
   }
   s.meta = take(2 * sizeof(P2Meta));
   s.red = take(8 * sizeof(double));  // one partial per producer warp
   s.amb = take(((kcap >> 5) + 1) * sizeof(uint32_t));
   s.item = take(sizeof(int64_t));
   s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
-  s.mrow = take(sizeof(int32_t) * 128);  // the consumer's winners: column (value path) / key hi, lo
   s.tab = take(sizeof(double) * (kcap + 2));  // alpha^m
   s.total = o;
   return s;
@@ -465,23 +491,39 @@ __device__ __forceinline__ void p2_sort_row(const T *row, int N, uint8_t *ord, i
   }
 }
 
+// W = Python's left-to-right sum (similarity.py:150) of the matched values of
+// rows 0..N-1, lane l holding rows l + 32 cc: the values are broadcast in row
+// order, every lane ends with the same sum (the dependent adds overlap the
+// shuffles instead of a lane-0 loop over shared memory)
+template <int KB>
+__device__ __forceinline__ double p2_row_sum(const double (&v)[KB], int N) {
+  double w = 0.0;
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++)
+    for (int l = 0; l < 32 && l + 32 * cc < N; l++) w += __shfl_sync(0xffffffffu, v[cc], l);
+  return w;
+}
+
 // Greedy rounds (similarity.py:96-108) on sorted rows, one warp: each round
 // takes the best current head over active rows (ties -> lowest row) and
-// advances the rows whose head column was taken.  Returns W (:150) on lane 0
-// (row-order sum), mrow[i] = matched column.
+// advances the rows whose head column was taken.  Returns W (:150), the
+// row-order sum (every lane).
 template <typename T, int KB>
-__device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uint8_t *ord, int32_t *mrow, int lane) {
+__device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uint8_t *ord, int lane) {
+  const int OP = p2_ord_pitch(N);
   int ptr[KB], ccol[KB];
   T cur[KB];
   bool act[KB];
   uint32_t taken[KB];
+  double win[KB];  // matched value of the lane's rows
 #pragma unroll
   for (int cc = 0; cc < KB; cc++) {
     const int i = lane + 32 * cc;
     act[cc] = i < N;
     ptr[cc] = 0;
     taken[cc] = 0u;
-    ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
+    win[cc] = 0.0;
+    ccol[cc] = act[cc] ? (int)ord[i * OP] : 0;
     cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
   }
   for (int round = 0; round < N; round++) {
@@ -500,10 +542,12 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
     for (int cc = 0; cc < KB; cc++)
       if (cc == (brow >> 5)) mycol = ccol[cc];
     const int bcol = __shfl_sync(0xffffffffu, mycol, brow & 31);
-    if (lane == 0) mrow[brow] = bcol;
 #pragma unroll
     for (int cc = 0; cc < KB; cc++) {
-      if (lane + 32 * cc == brow) act[cc] = false;
+      if (lane + 32 * cc == brow) {
+        act[cc] = false;
+        win[cc] = (double)cur[cc];
+      }
       if (cc == (bcol >> 5)) taken[cc] |= 1u << (bcol & 31);
     }
 #pragma unroll
@@ -514,7 +558,7 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
         bool tk;
         do {
           ++p;
-          col = ord[i * N + p];
+          col = ord[i * OP + p];
           uint32_t word = 0;
 #pragma unroll
           for (int q = 0; q < KB; q++)
@@ -527,11 +571,7 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
       }
     }
   }
-  __syncwarp();
-  double wsum = 0.0;
-  if (lane == 0)
-    for (int i = 0; i < N; i++) wsum += (double)Xs[i * P + mrow[i]];
-  return wsum;
+  return p2_row_sum<KB>(win, N);
 }
 
 // ---- exact packed keys: (value bits | 6-bit column field), comparable across
@@ -693,21 +733,24 @@ __device__ __forceinline__ void p2_row_order_pair(const unsigned long long *Krow
 // Greedy rounds on sorted key rows (pitch PK), one warp: a head's cross-row
 // key swaps the column field for (63 - row), so one 64-bit max picks the best
 // head with ties to the lowest row — np.argmax's first occurrence.
+#ifdef CFGSIM_P2_NOPREFETCH
 template <typename T, int KB>
 __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, const uint8_t *ord, int N, int emin,
-                                                 int32_t *mrow, int lane) {
+                                                 int lane) {
+  const int OP = p2_ord_pitch(N);
   unsigned long long hk[KB];
   int ptr[KB];
   bool act[KB];
   unsigned long long taken = 0ull;
+  unsigned long long win[KB];
 #pragma unroll
   for (int cc = 0; cc < KB; cc++) {
     const int i = lane + 32 * cc;
     act[cc] = i < N;
     ptr[cc] = 0;
-    hk[cc] = act[cc] ? Kr[i * PK + ord[i * N]] : 0ull;
+    win[cc] = 0ull;
+    hk[cc] = act[cc] ? Kr[i * PK + ord[i * OP]] : 0ull;
   }
-  double wsum = 0.0;
   for (int round = 0; round < N; round++) {
     unsigned long long g = 0ull;
 #pragma unroll
@@ -724,34 +767,104 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
       if ((brow >> 5) == cc) mine = hk[cc];
     const unsigned long long wk = __shfl_sync(0xffffffffu, mine, brow & 31);
     const int bcol = 63 - (int)(wk & 63ull);
-    if (lane == 0) {
-      mrow[2 * brow] = (int)(unsigned)(wk >> 32);  // winning key (value bits) for W
-      mrow[2 * brow + 1] = (int)(unsigned)wk;
-    }
     taken |= 1ull << bcol;
 #pragma unroll
     for (int cc = 0; cc < KB; cc++) {
-      if (lane + 32 * cc == brow) act[cc] = false;
+      if (lane + 32 * cc == brow) {
+        act[cc] = false;
+        win[cc] = hk[cc];
+      }
       if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
         const int i = lane + 32 * cc;
         int p = ptr[cc], col;
         do {
           ++p;
-          col = ord[i * N + p];
+          col = ord[i * OP + p];
         } while ((taken >> col) & 1ull);
         ptr[cc] = p;
         hk[cc] = Kr[i * PK + col];
       }
     }
   }
-  __syncwarp();
-  if (lane == 0)  // similarity.py:150: Python's sum, row order
-    for (int i = 0; i < N; i++) {
-      const unsigned long long k = ((unsigned long long)(unsigned)mrow[2 * i] << 32) | (unsigned)mrow[2 * i + 1];
-      wsum += p2_key_value<T>(k, emin);
-    }
-  return wsum;
+  double v[KB];
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++) v[cc] = lane + 32 * cc < N ? p2_key_value<T>(win[cc], emin) : 0.0;
+  return p2_row_sum<KB>(v, N);  // similarity.py:150: Python's sum, row order
 }
+#else
+template <typename T, int KB>
+__device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, const uint8_t *ord, int N, int emin,
+                                                 int lane) {
+  const int OP = p2_ord_pitch(N);
+  // per row: head key hk (position ptr) and the next position's column nc
+  // and key nk, loaded one advance ahead, so the common advance by one
+  // position (the next column is free) has no shared-memory load on the
+  // round's critical path
+  unsigned long long hk[KB], nk[KB];
+  int ptr[KB], nc[KB];
+  bool act[KB];
+  unsigned long long taken = 0ull;
+  unsigned long long win[KB];  // winning key of the lane's rows
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++) {
+    const int i = lane + 32 * cc;
+    act[cc] = i < N;
+    ptr[cc] = 0;
+    win[cc] = 0ull;
+    hk[cc] = act[cc] ? Kr[i * PK + ord[i * OP]] : 0ull;
+    nc[cc] = (act[cc] && N > 1) ? (int)ord[i * OP + 1] : 0;
+    nk[cc] = (act[cc] && N > 1) ? Kr[i * PK + nc[cc]] : 0ull;
+  }
+  for (int round = 0; round < N; round++) {
+    unsigned long long g = 0ull;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      const unsigned long long gk = (hk[cc] & ~63ull) | (unsigned long long)(63 - (lane + 32 * cc));
+      if (act[cc] && gk > g) g = gk;
+    }
+    const unsigned ghi = __reduce_max_sync(0xffffffffu, (unsigned)(g >> 32));
+    const unsigned glo = __reduce_max_sync(0xffffffffu, (unsigned)(g >> 32) == ghi ? (unsigned)g : 0u);
+    const int brow = 63 - (int)(glo & 63u);
+    unsigned long long mine = hk[0];
+#pragma unroll
+    for (int cc = 1; cc < KB; cc++)
+      if ((brow >> 5) == cc) mine = hk[cc];
+    const unsigned long long wk = __shfl_sync(0xffffffffu, mine, brow & 31);
+    const int bcol = 63 - (int)(wk & 63ull);
+    taken |= 1ull << bcol;
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++) {
+      if (lane + 32 * cc == brow) {
+        act[cc] = false;
+        win[cc] = hk[cc];
+      }
+      if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
+        const int i = lane + 32 * cc;
+        int p = ptr[cc] + 1;  // an active row always has an untaken column ahead
+        if ((taken >> nc[cc]) & 1ull) {
+          int col;
+          do {
+            ++p;
+            col = ord[i * OP + p];
+          } while ((taken >> col) & 1ull);
+          hk[cc] = Kr[i * PK + col];
+        } else {
+          hk[cc] = nk[cc];
+        }
+        ptr[cc] = p;
+        if (p + 1 < N) {  // next position, consumed at this row's next advance
+          nc[cc] = ord[i * OP + p + 1];
+          nk[cc] = Kr[i * PK + nc[cc]];
+        }
+      }
+    }
+  }
+  double v[KB];
+#pragma unroll
+  for (int cc = 0; cc < KB; cc++) v[cc] = lane + 32 * cc < N ? p2_key_value<T>(win[cc], emin) : 0.0;
+  return p2_row_sum<KB>(v, N);  // similarity.py:150: Python's sum, row order
+}
+#endif
 
 template <typename T, int KB, int AR, int BC, int PW, int MINB>
 __global__ void __launch_bounds__(32 * (PW + 1), MINB)
@@ -775,7 +888,6 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   if (warp == PW) {
     // ---------------- consumer: greedy rounds of the pairs in order
     // (a second consumer warp owning one buffer each measured 2% slower)
-    int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
     unsigned long long ph_t = 0;
     int ph_last = -1;
     for (int it = 0;; it++) {
@@ -788,8 +900,8 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       const T *Xs = (const T *)(smem_raw + L.x[s]);
       const double wsum =
           mt.keys ? p2_rounds_keys<T, KB>((const unsigned long long *)Xs, 32 * KB + 1, smem_raw + L.ord[s], N, mt.emin,
-                                          mrow, lane)
-                  : p2_rounds<T, KB>(Xs, P, N, smem_raw + L.ord[s], mrow, lane);
+                                          lane)
+                  : p2_rounds<T, KB>(Xs, P, N, smem_raw + L.ord[s], lane);
       if (lane == 0) {
         if (out.d) out.d[mt.slot] = isorank_distance_of(wsum, N);
         if (out.W) out.W[mt.slot] = wsum;
@@ -810,7 +922,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   for (int m = tid; m <= prm.kcap + 1; m += NP) apw[m] = prm.apow[m];  // alpha^m, once per CTA
   nbar_sync(BAR_P, NP);
   const int NPt = seq_pitch<T>(N);                      // history row pitch
-  const int SPD = ((2 * NPt + 7) / 16) * 16 + 8;        // staged row pitch (== 8 mod 16 doubles: 2-wavefront fragments)
+  const int SPD = p2_stage_pitch(NPt, (int)sizeof(T));  // staged row pitch (conflict-free fragment loads)
   unsigned long long ph_t = 0;
   int ph_last = -1;
   for (int it = 0;; it++) {
@@ -1049,12 +1161,12 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       if constexpr (KB == 2) {  // two adjacent lanes per row
         const int row = tid >> 1, half = tid & 1;
         const bool act = row < N;
-        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * N, half, act);
+        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * p2_ord_pitch(N), half, act);
       } else {
-        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * N);
+        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * p2_ord_pitch(N));
       }
     } else {
-      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * N, lane);
+      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * p2_ord_pitch(N), lane);
     }
     if (tid == 0) {
       meta[s].slot = slot;
