@@ -186,6 +186,17 @@ CFGSIM_API int cfgsim_flat_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B,
                                  const int32_t *ib, int32_t measure, double p, double *out, void *cuda_stream);
 CFGSIM_API int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, double p, double *d_mat,
                                     void *cuda_stream);
+/* `compare --measure all` (cli.py:154-164) for the five flat measures in ONE
+ * pass: d_mats = 5 consecutive K x K matrices in the order EUC, MAN, MIN, JAC,
+ * COS (CFGSIM_EUC..CFGSIM_COS), each exactly cfgsim_flat_allpairs' output for
+ * that measure (the six sums are formed from the same interpolated entries;
+ * EUC and JAC share sum (x-y)^2).  [host|device] output. */
+CFGSIM_API int cfgsim_flat_all_allpairs(const cfgsim_corpus *c, double p, double *d_mats, void *cuda_stream);
+
+/* Diagnostics (not on any alignment path): fp64 mma.sync.m8n8k4 and DFMA
+ * throughput of the device in TFLOP/s, measured now (bench.py's roofline
+ * denominator, at the clocks of the run). */
+CFGSIM_API int cfgsim_probe_fp64(int32_t device, double *mma_tflops, double *fma_tflops);
 
 /* export_heatmap_csv (similarity.py:287-293), native and multi-threaded (host
  * code; the K x K text for K = 20k is ~4 GB): ids = concatenated UTF-8

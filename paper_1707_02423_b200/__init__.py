@@ -27,7 +27,7 @@ _LAZY = {
     "loader": ("load_corpus_matrices", "load_manifest", "matrices_from_listings"),
     "similarity": ("AlignmentResult", "MeasureId", "PairwiseMatrix", "cosine", "euclidean", "export_heatmap_csv",
                    "isorank_align", "isorank_distance", "isorank_pairs", "jaccard", "manhattan", "measure_distance",
-                   "minkowski", "minmax_scale", "nearest", "pairwise"),
+                   "minkowski", "minmax_scale", "nearest", "pairwise", "pairwise_all"),
 }
 _WHERE = {name: mod for mod, names in _LAZY.items() for name in names}
 
@@ -52,7 +52,7 @@ __all__ = [
     "DimMismatch", "DuplicateKernel", "EmptyGraph", "GLOBAL", "INTERPOLATED", "MeasureId",
     "PairwiseMatrix", "RAW_COUNTS", "ROW_STOCHASTIC", "SasscfgError", "TransitionMatrix",
     "export_heatmap_csv", "interpolate_to", "isorank_align", "isorank_distance", "isorank_pairs",
-    "measure_distance", "minmax_scale", "nearest", "normalize_pair", "pack", "pairwise",
+    "measure_distance", "minmax_scale", "nearest", "normalize_pair", "pack", "pairwise", "pairwise_all",
     "euclidean", "manhattan", "minkowski", "jaccard", "cosine",
     "CorpusError", "ListingSyntaxError", "ProfileSyntaxError", "UnresolvedLabel",
     "load_corpus_matrices", "load_manifest", "matrices_from_listings",

@@ -67,6 +67,8 @@ _SIGS = {
     "cfgsim_flat_single": ([_i32, _i32, _vp, _i32, _vp, _i32, C.c_double, _vp], C.c_int),
     "cfgsim_flat_pairs": ([_vp, _vp, _i64, _vp, _vp, _i32, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_flat_allpairs": ([_vp, _i32, C.c_double, _vp, _vp], C.c_int),
+    "cfgsim_flat_all_allpairs": ([_vp, C.c_double, _vp, _vp], C.c_int),
+    "cfgsim_probe_fp64": ([_i32, _vp, _vp], C.c_int),
     "cfgsim_heatmap_csv": ([_i32, _vp, _vp, _vp, _vp, _i64, _vp, _i32], C.c_int),
     "cfgsim_ward": ([_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "cfgsim_matrices_from_listings": ([_i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.POINTER(_vp)], C.c_int),

@@ -21,13 +21,25 @@
 #include <vector>
 
 #include "../../include/cfgsim.h"
+#include <nvtx3/nvToolsExt.h>
 #include "isorank.cuh"
 #include "tiers.h"
 #include "isorank_lr.cuh"
 #include "flat.cuh"
 #include "ward.cuh"
+#include "isorank_start.cuh"
 
 using namespace cfgsim;
+
+// NVTX ranges (SURVEY §5 tracing): pack / stage 1 / stage 2 / large-N /
+// gather show up as named ranges under nsys or ncu --nvtx
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define CFGSIM_NVTX(name) NvtxRange nvtx_range_(name)
 
 namespace {
 
@@ -455,11 +467,16 @@ int big_kcap(double alpha, double tol, int max_iter) {
 }
 
 int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, const PairWork &work,
-               const PairOut &out, const cfgsim_params *p, unsigned long long *counter, cudaStream_t st) {
+               const PairOut &out, const cfgsim_params *p, unsigned long long *counter, cudaStream_t st,
+               const double *xg = nullptr, int kg = 0, int convg = 0) {
+  CFGSIM_NVTX("cfgsim.large_n");
   if (nlim > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(nlim) + " exceeds 1024");
   const int kb = big_kb(nlim);
   const void *fn = big_fn(precision, kb);
-  BigParams prm;
+  BigParams prm{};
+  prm.xg = xg;  // given-X mode (fp64 only): sort + match an X computed outside
+  prm.kg = kg;
+  prm.convg = convg;
   prm.alpha = p->alpha;
   prm.tol = (precision == CFGSIM_FP32) ? std::max(p->tol, p->tol_fp32) : p->tol;
   prm.eps = (precision == CFGSIM_FP32) ? 0.02 : 1e-6;
@@ -607,6 +624,7 @@ int seq_upload(Scratch &S, const SeqTable &tb, const SeqRun &rr, const cfgsim_pa
 template <typename T>
 int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr, const cfgsim_params *p, Scratch &S,
                cudaStream_t st, bool single = false) {
+  CFGSIM_NVTX("cfgsim.stage1");
   if (n <= 0) return CFGSIM_OK;
   int dev, sms = 0;
   CU(cudaGetDevice(&dev));
@@ -660,6 +678,7 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
 template <typename T>
 int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const PairOut &o, const SeqRun &rr,
                const cfgsim_params *p, Scratch &S, int &launch_no, cudaStream_t st) {
+  CFGSIM_NVTX("cfgsim.stage2");
   if (w.n_items <= 0) return CFGSIM_OK;
   int dev, sms = 0;
   CU(cudaGetDevice(&dev));
@@ -1301,6 +1320,7 @@ bool build_csc(int32_t n_graphs, const int32_t *n_nodes, const int64_t *rp_off, 
 int corpus_create_impl(int32_t device, int32_t n_graphs, const int32_t *n_nodes, const int64_t *rp_off,
                        const int32_t *rowptr, const int64_t *nz_off, const int32_t *col, const double *val,
                        const int32_t *cscp_in, const int32_t *crow_in, const double *cval_in, cfgsim_corpus **out) {
+  CFGSIM_NVTX("cfgsim.pack");
   if (!out || n_graphs < 1 || !n_nodes || !rp_off || !rowptr || !nz_off)
     return fail(CFGSIM_ERR_ARG, "bad corpus arguments");
   if (int rc = set_device(device)) return rc;
@@ -1496,6 +1516,7 @@ int cfgsim_corpus_info(const cfgsim_corpus *c, int32_t *n_graphs, int32_t *max_n
 int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_pairs,
                          const int32_t *ia, const int32_t *ib, const cfgsim_params *p, double *d,
                          double *W, int32_t *iters, uint8_t *converged, void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.isorank_pairs");
   if (!A || !B || n_pairs < 0 || (n_pairs && (!ia || !ib)))
     return fail(CFGSIM_ERR_ARG, "bad pair arguments");
   if (int rc = check_params(p)) return rc;
@@ -1565,6 +1586,7 @@ int cfgsim_allpairs_split(const cfgsim_corpus *c, int32_t world, int64_t *bounds
 int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_t ordered,
                           const cfgsim_params *p, double *d_lin, int32_t *iters_lin,
                           void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.allpairs_range");
   if (!c || u0 < 0 || u1 < u0 || u1 > c->row_start[c->K])
     return fail(CFGSIM_ERR_ARG, "bad unit range");
   if (int rc = check_params(p)) return rc;
@@ -1659,6 +1681,7 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
 int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const double *d_lin,
                             const int32_t *iters_lin, double *d_mat, int32_t *iters_mat,
                             void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.gather");
   if (!c || !d_lin || !d_mat) return fail(CFGSIM_ERR_ARG, "bad arguments");
   if (int rc = set_device(c->device)) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -1673,6 +1696,7 @@ int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const doubl
 
 int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params *p,
                     double *d_mat, int32_t *iters_mat, void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.allpairs");
   if (!c || !d_mat) return fail(CFGSIM_ERR_ARG, "bad arguments");
   if (int rc = check_params(p)) return rc;
   if (int rc = set_device(c->device)) return rc;
@@ -1699,10 +1723,91 @@ int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params
   return CFGSIM_OK;
 }
 
+// isorank_align(start=...) beyond the on-chip general kernel (N <= 1024):
+// the reference iteration with X in HBM (isorank_start.cuh), then the
+// large-N kernel's sort + matching on the final X.  fp64.
+int start_big_single(const cfgsim_corpus *ca, const cfgsim_corpus *cb, int N, const cfgsim_params *p,
+                     const double *dx0, double *dd, double *dw, int32_t *di, uint8_t *dc, double *dX, int32_t *dm) {
+  CFGSIM_NVTX("cfgsim.start_large_n");
+  if (N > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
+  const int64_t nn = (int64_t)N * N;
+  const int64_t chunk = 8192;
+  const int nparts = (int)((nn + chunk - 1) / chunk);
+  DBuf opA, opB, xa, fb, tb, part, dpart, dlt, dia, dib, dsl;
+  CU(opA.alloc(sizeof(double) * nn));
+  CU(opB.alloc(sizeof(double) * nn));
+  CU(xa.alloc(sizeof(double) * nn));
+  CU(fb.alloc(sizeof(double) * nn));
+  CU(tb.alloc(sizeof(double) * nn));
+  CU(part.alloc(sizeof(double) * nparts));
+  CU(dpart.alloc(sizeof(double) * nparts));
+  CU(dlt.alloc(sizeof(double)));
+  cudaStream_t st = 0;
+  const DevCorpus A = ca->dev(), B = cb->dev();
+  start_dense_op_kernel<<<(N + 7) / 8, 256, 0, st>>>(A, 0, N, opA.as<double>());
+  start_dense_op_kernel<<<(N + 7) / 8, 256, 0, st>>>(B, 0, N, opB.as<double>());
+  g_launches += 2;
+  CU(cudaMemcpyAsync(xa.p, dx0, sizeof(double) * nn, cudaMemcpyDeviceToDevice, st));
+  const dim3 gg((N + SG_T - 1) / SG_T, (N + SG_T - 1) / SG_T);
+  const double u = 1.0 / (double)nn;  // np.full(n * n, 1.0 / (n * n))
+  int k = 0, conv = 0;
+  for (k = 1; k <= p->max_iter; k++) {
+    start_gemm_kernel<<<gg, 256, 0, st>>>(opA.as<double>(), xa.as<double>(), tb.as<double>(), N, 1);  // A'^T X
+    start_gemm_kernel<<<gg, 256, 0, st>>>(tb.as<double>(), opB.as<double>(), fb.as<double>(), N, 0);  // (.) B'
+    start_update_kernel<<<nparts, SR_T, 0, st>>>(fb.as<double>(), nn, p->alpha, u, chunk, part.as<double>());
+    start_norm_kernel<<<nparts, SR_T, 0, st>>>(fb.as<double>(), xa.as<double>(), nn, chunk, part.as<double>(), nparts,
+                                               dpart.as<double>());
+    start_delta_kernel<<<1, 32, 0, st>>>(dpart.as<double>(), nparts, dlt.as<double>());
+    g_launches += 5;
+    CU(cudaGetLastError());
+    double delta = 0.0;
+    CU(cudaMemcpyAsync(&delta, dlt.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    std::swap(xa.p, fb.p);  // x = fresh (similarity.py:143)
+    if (delta < p->tol) {   // :144
+      conv = 1;
+      break;
+    }
+  }
+  if (k > p->max_iter) k = p->max_iter;
+  if (dX) CU(cudaMemcpyAsync(dX, xa.p, sizeof(double) * nn, cudaMemcpyDeviceToDevice, st));
+  int32_t zero = 0;
+  int64_t zslot = 0;
+  CU(dia.alloc(sizeof(int32_t)));
+  CU(dib.alloc(sizeof(int32_t)));
+  CU(dsl.alloc(sizeof(int64_t)));
+  CU(cudaMemcpyAsync(dia.p, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dib.p, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dsl.p, &zslot, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  PairWork w{};
+  w.mode = WORK_LIST;
+  w.n_items = 1;
+  w.ia = dia.as<int32_t>();
+  w.ib = dib.as<int32_t>();
+  w.slot = dsl.as<int64_t>();
+  PairOut o{};
+  o.d = dd;
+  o.W = dw;
+  o.iters = di;
+  o.conv = dc;
+  o.match = dm;
+  Scratch &S = scratch_for(ca->device);
+  if (int rc = ensure_scratch(S, 1 << 16)) return rc;
+  cfgsim_params p64 = *p;
+  p64.precision = CFGSIM_FP64;
+  if (int rc = big_launch(CFGSIM_FP64, N, A, B, w, o, &p64, S.counters.as<unsigned long long>(), st, xa.as<double>(), k,
+                          conv))
+    return rc;
+  if (int rc = big_status(S, st)) return rc;
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
 int cfgsim_isorank_single(int32_t device, int32_t na, const double *A, int32_t nb,
                           const double *B, const cfgsim_params *p, const double *x0,
                           double *X_out, int32_t *match_out, double *d, double *W,
                           int32_t *iters, uint8_t *converged) {
+  CFGSIM_NVTX("cfgsim.isorank_single");
   if (na < 1 || nb < 1 || !A || !B) return fail(CFGSIM_ERR_ARG, "bad matrices");
   if (int rc = check_params(p)) return rc;
   if (int rc = set_device(device)) return rc;
@@ -1731,7 +1836,11 @@ int cfgsim_isorank_single(int32_t device, int32_t na, const double *A, int32_t n
     cu(dx0.alloc(sizeof(double) * N * N));
     cu(cudaMemcpy(dx0.p, x0, sizeof(double) * N * N, cudaMemcpyHostToDevice));
   }
-  if (rc == CFGSIM_OK) {
+  if (rc == CFGSIM_OK && x0 && plan_for(p->precision, N, false).ti < 0) {
+    // a start vector beyond the on-chip general kernel's tiers
+    rc = start_big_single(ca, cb, N, p, dx0.as<double>(), dd.as<double>(), dw.as<double>(), di.as<int32_t>(),
+                          dc.as<uint8_t>(), dX.as<double>(), dm.as<int32_t>());
+  } else if (rc == CFGSIM_OK) {
     std::vector<int32_t> ia{0}, ib{0};
     std::vector<int64_t> sl{0};
     rc = run_list(ca, cb, ia, ib, sl, p, dd.as<double>(), dw.as<double>(), di.as<int32_t>(),
@@ -1753,6 +1862,7 @@ int cfgsim_isorank_single(int32_t device, int32_t na, const double *A, int32_t n
 
 int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, int32_t c1,
                    const cfgsim_params *p, double *best_d, int64_t *best_idx, void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.nearest");
   if (!Q || !C || c0 < 0 || c1 > C->K || c1 <= c0 || !best_d || !best_idx)
     return fail(CFGSIM_ERR_ARG, "bad nearest arguments");
   if (int rc = check_params(p)) return rc;
@@ -1929,6 +2039,7 @@ int cfgsim_interpolate(int32_t device, int32_t n, const double *src, int32_t tar
 
 int cfgsim_flat_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_pairs, const int32_t *ia,
                       const int32_t *ib, int32_t measure, double p, double *out, void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.flat_pairs");
   if (!A || !B || n_pairs < 0 || (n_pairs && (!ia || !ib || !out))) return fail(CFGSIM_ERR_ARG, "bad pair arguments");
   if (A->device != B->device) return fail(CFGSIM_ERR_ARG, "corpora live on different devices");
   if (int rc = set_device(A->device)) return rc;
@@ -1965,6 +2076,7 @@ int cfgsim_flat_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t n_
 }
 
 int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, double p, double *d_mat, void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.flat_allpairs");
   if (!c || !d_mat) return fail(CFGSIM_ERR_ARG, "bad arguments");
   if (int rc = set_device(c->device)) return rc;
   const bool bad_order = measure == CFGSIM_MIN && !(p >= 1.0);
@@ -1984,6 +2096,101 @@ int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, double p, doub
   if (int rc = flat_launch(c, c, w, (double *)so.dev, st)) return rc;
   CU(so.finish(st));
   CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+int cfgsim_flat_all_allpairs(const cfgsim_corpus *c, double p, double *d_mats, void *cuda_stream) {
+  CFGSIM_NVTX("cfgsim.flat_all_allpairs");
+  if (!c || !d_mats) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  if (int rc = set_device(c->device)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t KK = (size_t)c->K * c->K;
+  OutStage so;
+  CU(so.prepare(d_mats, 5 * sizeof(double) * KK));
+  CU(cudaMemsetAsync(so.dev, 0, 5 * sizeof(double) * KK, st));  // definitional zero diagonals (similarity.py:248-255)
+  FlatWork w{};
+  w.mode = 1;
+  w.n_items = (int64_t)c->K * (c->K - 1) / 2;
+  w.K = c->K;
+  w.measure = FLAT_ALL;
+  w.p = p;  // p < 1: the MIN matrix is all NaN (BadOrder caught per pair, :243-246)
+  w.out_stride = (int64_t)KK;
+  if (int rc = flat_launch(c, c, w, (double *)so.dev, st)) return rc;
+  CU(so.finish(st));
+  CU(cudaStreamSynchronize(st));
+  return CFGSIM_OK;
+}
+
+namespace {
+// fp64 peak probes (the roofline denominator, measured in the same process
+// and at the same clocks as the bench): independent accumulator chains, so
+// the pipe, not latency, limits.  Not part of any alignment path.
+__global__ void probe_dmma_kernel(double *out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+  for (int t = 0; t < 8; t++) c[t][0] = c[t][1] = t;
+  for (int i = 0; i < iters; i++)
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[t][0]), "+d"(c[t][1])
+                   : "d"(a), "d"(b));
+  double s = 0;
+  for (int t = 0; t < 8; t++) s += c[t][0] + c[t][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void probe_dfma_kernel(double *out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[16];
+  for (int t = 0; t < 16; t++) c[t] = t;
+  for (int i = 0; i < iters; i++)
+#pragma unroll
+    for (int t = 0; t < 16; t++) c[t] = fma(a, b, c[t]);
+  double s = 0;
+  for (int t = 0; t < 16; t++) s += c[t];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+int cfgsim_probe_fp64(int32_t device, double *mma_tflops, double *fma_tflops) {
+  if (int rc = set_device(device)) return rc;
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int blocks = sms * 8, threads = 256, iters = 2048;
+  DBuf out;
+  CU(out.alloc(sizeof(double) * blocks * threads));
+  cudaStream_t st;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  auto time_it = [&](bool mma, double *res) -> int {
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; rep++) {
+      CU(cudaEventRecord(e0, st));
+      if (mma) probe_dmma_kernel<<<blocks, threads, 0, st>>>(out.as<double>(), iters);
+      else probe_dfma_kernel<<<blocks, threads, 0, st>>>(out.as<double>(), iters);
+      CU(cudaEventRecord(e1, st));
+      CU(cudaEventSynchronize(e1));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    // dmma: 8 mma m8n8k4 (512 flop each) per warp per iteration; dfma: 16 fma (2 flop) per thread
+    const double flops = mma ? (double)blocks * (threads / 32) * iters * 8 * 512.0
+                             : (double)blocks * threads * iters * 16 * 2.0;
+    *res = flops / (best * 1e-3) / 1e12;
+    return CFGSIM_OK;
+  };
+  double m = 0, f = 0;
+  int rc = time_it(true, &m);
+  if (rc == CFGSIM_OK) rc = time_it(false, &f);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  if (rc) return rc;
+  if (mma_tflops) *mma_tflops = m;
+  if (fma_tflops) *fma_tflops = f;
   return CFGSIM_OK;
 }
 
@@ -2063,6 +2270,7 @@ int cfgsim_heatmap_csv(int32_t k, const char *ids, const int64_t *id_off, const 
 
 int cfgsim_ward(int32_t device, int32_t k, int32_t dim, const double *features, int64_t *out_a, int64_t *out_b,
                 double *out_d, int64_t *out_size) {
+  CFGSIM_NVTX("cfgsim.ward");
   // ward_linkage (cluster.py:88-134) on the GPU: k feature vectors of length
   // dim (row-major host array); k - 1 merges (a < b ids, distance, size).
   if (k < 2 || dim < 0 || (dim && !features) || !out_a || !out_b || !out_d || !out_size)

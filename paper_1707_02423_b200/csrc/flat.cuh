@@ -21,7 +21,7 @@
 
 namespace cfgsim {
 
-enum { FLAT_EUC = 0, FLAT_MAN = 1, FLAT_MIN = 2, FLAT_JAC = 3, FLAT_COS = 4 };
+enum { FLAT_EUC = 0, FLAT_MAN = 1, FLAT_MIN = 2, FLAT_JAC = 3, FLAT_COS = 4, FLAT_ALL = 5 };
 constexpr int FLAT_THREADS = 128;
 
 struct FlatWork {
@@ -32,7 +32,13 @@ struct FlatWork {
   int32_t measure;
   double p;
   int32_t nlim;       // max source size (shared row buffers)
+  int64_t out_stride; // FLAT_ALL: measure m's outputs at out + m * out_stride
 };
+
+// FLAT_ALL (`compare --measure all`, cli.py:154-164): the five measures from
+// ONE walk over each pair's size-normalised entries — the six sums share
+// every interpolated entry, so the five reference pairwise() passes
+// (similarity.py:247-255 per measure) become one kernel pass.
 
 // source side of one pair: dense rows staged on demand
 struct FlatSide {
@@ -130,6 +136,9 @@ __global__ void __launch_bounds__(FLAT_THREADS)
         const double y = flat_value(SB, rows + 2 * L, rows + 3 * L, fb, q);
         const double d = x - y, ad = fabs(d);
         switch (work.measure) {
+          case FLAT_ALL:  // (x-y)^2 == |x-y|^2 exactly, so EUC and JAC share s2
+            s2 += ad * ad; s1 += ad; sp += pow(ad, work.p); sxx += x * x; syy += y * y; sxy += x * y;
+            break;
           case FLAT_EUC: s2 += ad * ad; break;
           case FLAT_MAN: s1 += ad; break;
           case FLAT_MIN: sp += pow(ad, work.p); break;
@@ -152,24 +161,32 @@ __global__ void __launch_bounds__(FLAT_THREADS)
         t[k] = 0.0;
         for (int w = 0; w < FLAT_THREADS / 32; w++) t[k] += red[k][w];
       }
-      double r;
-      switch (work.measure) {
-        case FLAT_EUC: r = sqrt(t[0]); break;
-        case FLAT_MAN: r = t[1]; break;
-        case FLAT_MIN: r = work.p >= 1.0 ? pow(t[2], 1.0 / work.p) : CUDART_NAN; break;  // BadOrder
-        case FLAT_JAC: {
-          const double den = t[3] + t[4] - t[5];
-          r = den == 0.0 ? CUDART_NAN : t[0] / den;  // DegenerateInput
-          break;
+      auto value = [&](int m) {
+        switch (m) {
+          case FLAT_EUC: return sqrt(t[0]);
+          case FLAT_MAN: return t[1];
+          case FLAT_MIN: return work.p >= 1.0 ? pow(t[2], 1.0 / work.p) : CUDART_NAN;  // BadOrder
+          case FLAT_JAC: {
+            const double den = t[3] + t[4] - t[5];
+            return den == 0.0 ? CUDART_NAN : t[0] / den;  // DegenerateInput
+          }
+          default: {
+            const double nx = sqrt(t[3]), ny = sqrt(t[4]);
+            return (nx == 0.0 || ny == 0.0) ? CUDART_NAN : 1.0 - t[5] / (nx * ny);  // DegenerateInput
+          }
         }
-        default: {
-          const double nx = sqrt(t[3]), ny = sqrt(t[4]);
-          r = (nx == 0.0 || ny == 0.0) ? CUDART_NAN : 1.0 - t[5] / (nx * ny);  // DegenerateInput
-          break;
+      };
+      if (work.measure == FLAT_ALL) {
+        for (int m = 0; m < 5; m++) {
+          const double r = value(m);
+          out[m * work.out_stride + o1] = r;
+          if (o2 >= 0) out[m * work.out_stride + o2] = r;
         }
+      } else {
+        const double r = value(work.measure);
+        out[o1] = r;
+        if (o2 >= 0) out[o2] = r;
       }
-      out[o1] = r;
-      if (o2 >= 0) out[o2] = r;
     }
     __syncthreads();
   }

@@ -51,6 +51,11 @@ struct BigParams {
   int64_t slab_bytes;  // per CTA
   int32_t *status;     // != 0: internal error (history overflow)
   unsigned long long *phase;  // optional (CFGSIM_PHASES=1): cycles per phase, summed over CTAs
+  // given-X mode (isorank_align(start=...) for N > 128): X after the sweeps
+  // was computed outside (isorank_start.cuh); the kernel only sorts and
+  // matches it.  One pair, fp64.
+  const double *xg;
+  int32_t kg, convg;
 };
 
 // per-CTA global slab
@@ -91,7 +96,7 @@ struct BigSmem {
   // sort region: one staged X row per warp
   size_t rows;
   // greedy region
-  size_t hold, dfl, taken, gslot, mrow, mval;
+  size_t taken, gslot, mrow, mval;
   size_t red, misc, total;
 };
 
@@ -126,9 +131,7 @@ __host__ __device__ inline BigSmem big_smem_layout(int nlim) {
   s.rows = take(sizeof(T) * BIG_WARPS * (size_t)big_row_pitch(nlim));
   const size_t sort_end = o;
   o = base;
-  s.hold = take(2 * sizeof(unsigned long long) * nlim);  // per column: (value bits, 0xffff - row)
-  s.dfl = take(sizeof(uint8_t) * nlim);                  // per row: displaced in this step
-  s.taken = take(sizeof(uint32_t) * 64);  // (CFGSIM_BIG_ROUNDS) two generations of taken columns
+  s.taken = take(sizeof(uint32_t) * 64);  // two generations of taken columns
   s.gslot = take(sizeof(unsigned long long) * 2 * BIG_WARPS + sizeof(int32_t) * (4 * BIG_WARPS + 2));
   s.mrow = take(sizeof(int32_t) * nlim);
   s.mval = take(sizeof(unsigned long long) * nlim);
@@ -294,20 +297,6 @@ __device__ __forceinline__ int big_key_col(unsigned long long k) {
   return (1 << BIG_CB) - 1 - (int)(k & ((1ull << BIG_CB) - 1));
 }
 
-// 16-byte compare-and-swap in shared memory (sm_90+): {lo, hi} at addr
-__device__ __forceinline__ void big_cas128(unsigned long long *addr, unsigned long long cmp_lo,
-                                           unsigned long long cmp_hi, unsigned long long new_lo,
-                                           unsigned long long new_hi, unsigned long long &old_lo,
-                                           unsigned long long &old_hi) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(addr);
-  asm volatile(
-      "{\n .reg .b128 d, b, c;\n mov.b128 b, {%2, %3};\n mov.b128 c, {%4, %5};\n"
-      " atom.shared.cas.b128 d, [%6], b, c;\n mov.b128 {%0, %1}, d;\n}\n"
-      : "=l"(old_lo), "=l"(old_hi)
-      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "r"(a)
-      : "memory");
-}
-
 __device__ __forceinline__ void big_cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // B-byte async copy global -> shared; zero-fills the destination when !valid
@@ -396,7 +385,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
   T *coef = (T *)(slab + G.coef);
   T *Uh = (T *)(slab + G.uh);
   T *Vh = (T *)(slab + G.vh);
-  T *X = (T *)(slab + G.x);
+  T *X = prm.xg ? (T *)prm.xg : (T *)(slab + G.x);
   unsigned long long *sval = (unsigned long long *)(slab + G.sval);
   uint16_t *scol = (uint16_t *)(slab + G.scol);
   double *red = (double *)(smem_raw + L.red);
@@ -423,6 +412,18 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       const int na = C1.n_nodes[g1], nb = C2.n_nodes[g2];
       const int N = na > nb ? na : nb;
 
+      int it_done = prm.max_iter;
+      bool converged = false;
+      int emin = 0x7fffffff, emax = -1;
+      if (prm.xg) {  // given X: its exponent range only
+        it_done = prm.kg;
+        converged = prm.convg != 0;
+        for (int e = tid; e < N * N; e += NT) {
+          const int x = big_exponent(X[e]);
+          emin = min(emin, x);
+          emax = max(emax, x);
+        }
+      } else {
       BIG_PHASE(0);
       // ---- 1. operators
       BigSide SA, SB;
@@ -461,8 +462,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       const double inv_nn = 1.0 / (double)((long long)N * N);
       const double c = (1.0 - prm.alpha) * inv_nn;  // (1-alpha)*uniform, similarity.py:140
       double ak1 = 1.0;                             // alpha^(k-1)
-      int it_done = prm.max_iter;
-      bool converged = false;
       int k = 1;
       __syncthreads();
       for (;; k++) {
@@ -583,7 +582,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       //         low-rank kernel forms as cak * u).
       for (int e = tid; e < (K + 1) * N; e += NT) Uh[e] = coef[e / N] * Uh[e];
       __syncthreads();
-      int emin = 0x7fffffff, emax = -1;
       {
         T *Us = (T *)(smem_raw + L.us);
         T *Vs = (T *)(smem_raw + L.vs);
@@ -717,6 +715,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
             }
         }
       }
+      }  // (phases 1-3)
       {
         int *ered = (int *)(smem_raw + L.misc + 32);
         emin = __reduce_min_sync(0xffffffffu, emin);
@@ -747,36 +746,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       // order; equal 22-bit prefixes with different exact values (near-ties,
       // ~1e-6 relative) are repaired by odd-even transposition on the exact
       // keys.  Exactly tied values keep column order from the key's low bits.
-#ifdef CFGSIM_BIG_NOSTAGE
-#define BIG_RP(e) (e)
-      for (int i = warp; i < N; i += BIG_WARPS) {
-        const T *row = X + (size_t)i * N;
-        int rmin = 0x7fffffff, rmax = -1;
-        for (int j = lane; j < N; j += 32) {
-          const int e = big_exponent(row[j]);
-          rmin = min(rmin, e);
-          rmax = max(rmax, e);
-        }
-        rmin = __reduce_min_sync(0xffffffffu, rmin);
-        rmax = __reduce_max_sync(0xffffffffu, rmax);
-        constexpr int MB = sizeof(T) == 8 ? 52 : 23;
-        const int rshift = (32 - __clz(rmax - rmin)) + MB - 22;  // value bits above the 22 kept
-        uint32_t key[KB];
-#pragma unroll
-        for (int c = 0; c < KB; c++) {
-          const int j = lane * KB + c;
-          uint32_t k = 0u;  // padding sorts last (a real key's column field is >= 1024 - N >= 1 then)
-          if (j < N) {
-            const unsigned long long b = big_bits(row[j]);
-            const unsigned long long v =
-                ((((b >> MB) & (sizeof(T) == 8 ? 0x7ffull : 0xffull)) - (unsigned long long)rmin) << MB) |
-                (b & ((1ull << MB) - 1));
-            k = ((uint32_t)(v >> rshift) << BIG_CB) | (uint32_t)((1 << BIG_CB) - 1 - j);
-          }
-          key[c] = k;
-        }
-#else
-#define BIG_RP(e) big_rpos(e)
       T *rbuf = (T *)(smem_raw + L.rows) + (size_t)warp * big_row_pitch(prm.nlim);
       for (int i = warp; i < N; i += BIG_WARPS) {
         // row i staged in shared memory with one coalesced pass (the sort's
@@ -812,7 +781,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           }
           key[c] = k;
         }
-#endif
         big_sort_desc<uint32_t, KB>(key, lane);
         // pair-wide 64-bit keys (exponent | mantissa truncated by `shift` bits |
         // column) in sorted order; odd-even transposition repairs inversions
@@ -823,7 +791,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         for (int c = 0; c < KB; c++) {
           const int pos = lane * KB + c;
           const int col = (1 << BIG_CB) - 1 - (int)(key[c] & ((1u << BIG_CB) - 1));
-          ek[c] = (pos < N) ? big_sort_key<T>(row[BIG_RP(col)], col, emin, shift) : 0ull;
+          ek[c] = (pos < N) ? big_sort_key<T>(row[big_rpos(col)], col, emin, shift) : 0ull;
         }
         // `after(x, y)`: y must precede x — (value desc, column asc), exact:
         // equal truncated values are decided on X (keys' low bits only hold
@@ -831,7 +799,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         auto after = [&](unsigned long long x, unsigned long long y) {
           if ((x >> BIG_CB) != (y >> BIG_CB)) return (x >> BIG_CB) < (y >> BIG_CB);
           if (shift > 0) {
-            const T vx = row[BIG_RP(big_key_col(x))], vy = row[BIG_RP(big_key_col(y))];
+            const T vx = row[big_rpos(big_key_col(x))], vy = row[big_rpos(big_key_col(y))];
             if (vx != vy) return vx < vy;
           }
           return (x & ((1ull << BIG_CB) - 1)) < (y & ((1ull << BIG_CB) - 1));  // lower column first
@@ -861,7 +829,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           const int pos = lane * KB + c;
           if (pos < N) {
             const int col = big_key_col(ek[c]);
-            ov[pos] = big_bits(row[BIG_RP(col)]);  // exact value bits for the matching
+            ov[pos] = big_bits(row[big_rpos(col)]);  // exact value bits for the matching
             oc[pos] = (uint16_t)col;
           }
         }
@@ -870,7 +838,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       __syncthreads();
 
       BIG_PHASE(4);
-#ifdef CFGSIM_BIG_ROUNDS
       // ---- 4b. greedy matching rounds, similarity.py:96-108, whole CTA.
       // Thread t owns rows t + 256 r (r < BIG_R); each active row's head is
       // its best untaken column, compared across rows on exact value bits
@@ -995,169 +962,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
             }
           }
         }
-#else
-      // ---- 4b. greedy matching, similarity.py:96-108, whole CTA, as
-      // row-proposing deferred acceptance (Gale-Shapley).  With edges
-      // totally ordered by (value desc, row asc, column asc) — the order in
-      // which np.argmax's first occurrence takes them — the greedy matching
-      // is the unique stable matching of rows and columns ranking each other
-      // by that order, so GS returns exactly it, in any proposal order.
-      // Rows walk their sorted orders; column c keeps the best proposal in a
-      // 16-byte (exact value bits, 0xffff - row) slot updated by 128-bit CAS;
-      // a displaced row resumes after the column it lost.  No per-round
-      // argmax or barrier: each thread's rows propose independently (their
-      // next sorted entries prefetched in registers), and a step only hands
-      // the displaced rows back to their owners.
-      {
-        unsigned long long *hold = (unsigned long long *)(smem_raw + L.hold);
-        uint8_t *dfl = (uint8_t *)(smem_raw + L.dfl);
-        int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
-        unsigned long long *mval = (unsigned long long *)(smem_raw + L.mval);
-        for (int c = tid; c < N; c += NT) {
-          hold[2 * c] = 0ull;  // free: (0, 0) loses to every real entry (values > 0)
-          hold[2 * c + 1] = 0ull;
-          dfl[c] = 0;
-        }
-        constexpr int PF = 3;  // prefetch depth (positions ahead of the head)
-        unsigned long long hv[BIG_R], qv[BIG_R][PF];
-        int hc[BIG_R], qc[BIG_R][PF], ptr[BIG_R];
-        uint32_t fr = 0u;  // rows of this thread without a column
-#pragma unroll
-        for (int r = 0; r < BIG_R; r++) {
-          const int i = tid + BIG_THREADS * r;
-          hv[r] = 0ull;
-          hc[r] = 0;
-          ptr[r] = 0;
-#pragma unroll
-          for (int f = 0; f < PF; f++) { qv[r][f] = 0ull; qc[r][f] = 0; }
-          if (i < N) {
-            fr |= 1u << r;
-            hv[r] = sval[(size_t)i * N];
-            hc[r] = scol[(size_t)i * N];
-#pragma unroll
-            for (int f = 0; f < PF; f++)
-              if (1 + f < N) {
-                qv[r][f] = sval[(size_t)i * N + 1 + f];
-                qc[r][f] = scol[(size_t)i * N + 1 + f];
-              }
-          }
-        }
-        // next sorted entry of row r (its head moves one position)
-        auto advance = [&](int r) {
-          const int i = tid + BIG_THREADS * r;
-          const int p = ++ptr[r];
-          hv[r] = qv[r][0];
-          hc[r] = qc[r][0];
-#pragma unroll
-          for (int f = 0; f + 1 < PF; f++) { qv[r][f] = qv[r][f + 1]; qc[r][f] = qc[r][f + 1]; }
-          if (p + PF < N) {
-            qv[r][PF - 1] = sval[(size_t)i * N + p + PF];
-            qc[r][PF - 1] = scol[(size_t)i * N + p + PF];
-          }
-        };
-#ifdef CFGSIM_BIG_GS_STEP
-        __syncthreads();
-        unsigned long long props = 0ull;
-        for (int step = 0;; step++) {
-          while (fr) {
-#pragma unroll
-            for (int r = 0; r < BIG_R; r++) {
-              if ((fr >> r) & 1u) {
-                const int i = tid + BIG_THREADS * r;
-                const unsigned long long v = hv[r], rc = (unsigned long long)(0xffff - i);
-                unsigned long long *slot = hold + 2 * hc[r];
-                unsigned long long ev = 0ull, er = 0ull, ov, orr;
-                bool won;
-                ++props;
-                for (;;) {
-                  big_cas128(slot, ev, er, v, rc, ov, orr);
-                  if (ov == ev && orr == er) { won = true; break; }
-                  if (ov > v || (ov == v && orr > rc)) { won = false; break; }
-                  ev = ov;
-                  er = orr;
-                }
-                if (won) {
-                  fr &= ~(1u << r);
-                  mrow[i] = hc[r];
-                  mval[i] = v;
-                  if (ov) dfl[0xffff - (int)orr] = 1;
-                } else {
-                  advance(r);
-                }
-              }
-            }
-          }
-          __syncthreads();
-          int mine = 0;
-#pragma unroll
-          for (int r = 0; r < BIG_R; r++) {
-            const int i = tid + BIG_THREADS * r;
-            if (i < N && dfl[i]) {
-              dfl[i] = 0;
-              fr |= 1u << r;
-              advance(r);
-              mine = 1;
-            }
-          }
-          if (!__syncthreads_or(mine)) break;
-        }
-#else
-        int *nheld = (int *)(smem_raw + L.misc + 96);  // columns with a holder
-        if (tid == 0) *nheld = 0;
-        __syncthreads();
-        unsigned long long props = 0ull;
-        // fully asynchronous: a thread proposes for its free rows, takes back
-        // rows another thread displaced (flag dfl), and spins until every
-        // column has a holder (then every row holds one: N rows, N columns)
-        for (;;) {
-          bool did = false;
-#pragma unroll
-          for (int r = 0; r < BIG_R; r++) {
-            const int i = tid + BIG_THREADS * r;
-            if (i < N && ((volatile uint8_t *)dfl)[i]) {
-              dfl[i] = 0;
-              fr |= 1u << r;
-              advance(r);
-            }
-          }
-          while (fr) {
-            did = true;
-#pragma unroll
-            for (int r = 0; r < BIG_R; r++) {
-              if ((fr >> r) & 1u) {
-                const int i = tid + BIG_THREADS * r;
-                const unsigned long long v = hv[r], rc = (unsigned long long)(0xffff - i);
-                unsigned long long *slot = hold + 2 * hc[r];
-                unsigned long long ev = 0ull, er = 0ull, ov, orr;
-                bool won;
-                ++props;
-                for (;;) {
-                  big_cas128(slot, ev, er, v, rc, ov, orr);
-                  if (ov == ev && orr == er) { won = true; break; }
-                  if (ov > v || (ov == v && orr > rc)) { won = false; break; }
-                  ev = ov;
-                  er = orr;
-                }
-                if (won) {
-                  fr &= ~(1u << r);
-                  mrow[i] = hc[r];
-                  mval[i] = v;
-                  if (ov) ((volatile uint8_t *)dfl)[0xffff - (int)orr] = 1;  // the previous holder is free again
-                  else atomicAdd(nheld, 1);
-                } else {
-                  advance(r);
-                }
-              }
-            }
-          }
-          if (*(volatile int *)nheld >= N) break;
-          if (!did) __nanosleep(32);
-        }
-        __syncthreads();
-#endif
-        if (prm.phase) atomicAdd(prm.phase + 5, props);  // diagnostics: proposals
-        if (prm.phase && tid == 0) atomicAdd(prm.phase + 7, (unsigned long long)N);
-#endif
         __syncthreads();
         if (tid == 0) {  // similarity.py:150: Python sum in row order
           double wsum = 0.0;

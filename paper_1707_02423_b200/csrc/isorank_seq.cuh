@@ -353,6 +353,7 @@ struct Pair2Params {
 // buffer, bar.sync / bar.arrive), so the sequential rounds overlap the GEMM
 // and sorts of the next pair.
 constexpr int P2_KC = 8;    // sweeps per staged chunk
+constexpr int P2_NS = 3;    // staging ring depth (chunks in flight while one is consumed)
 constexpr int P2_KMAX = 512;  // kcap bound of the two-stage path (host checks)
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
@@ -366,7 +367,7 @@ struct P2Meta {
 };
 
 struct P2Smem {
-  size_t x[2], ord[2], meta, red, amb, item, first, tab, total;
+  size_t x[2], ord[2], meta, red, amb, item, first, mrow, tab, total;
 };
 
 // staged history row pitch (elements; holds u_m and v_m side by side, >= 2
@@ -374,26 +375,10 @@ struct P2Smem {
 // column lr) are conflict-free: fp64 — a 64-bit request is served per
 // half-warp, and 2 pitch mod 32 banks must be 8 or 24 so that the four rows
 // lk land in disjoint bank octets (pitch == 4 mod 16; pitch == 8 mod 16 put
-// rows 0 and 2 on the same banks: 2-way conflicts, measured);  fp32 — rows
-// at pitch == 8 mod 16 floats start on bank octets 0/8/16/24.
+// rows 0 and 2 on the same banks: 2-way conflicts, ncu-measured);  fp32 —
+// rows at pitch == 8 mod 16 floats start on bank octets 0/8/16/24.
 __host__ __device__ inline int p2_stage_pitch(int npt, int tsize) {
-#ifdef CFGSIM_SPD_OLD
-  return ((2 * npt + 7) / 16) * 16 + 8;
-#else
   return tsize == 8 ? ((2 * npt + 11) / 16) * 16 + 4 : ((2 * npt + 7) / 16) * 16 + 8;
-#endif
-}
-
-// row-order pitch in bytes: an odd number of 4-byte words, so the rows a
-// warp touches at one position (one row per lane) fall in distinct banks
-// (pitch N put 16-32 rows in one bank: 8-16-way conflicts on every order
-// write and on the consumer's head reads)
-__host__ __device__ inline int p2_ord_pitch(int N) {
-#ifdef CFGSIM_ORD_NOPAD
-  return N;
-#else
-  return 4 * (((N + 3) / 4) | 1);
-#endif
 }
 
 __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
@@ -404,19 +389,21 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
     o += (b + 15) & ~size_t(15);
     return at;
   };
-  const int npt = (N + 3) & ~3, spd = p2_stage_pitch(npt, 8) > p2_stage_pitch(npt, 4) ? p2_stage_pitch(npt, 8) : p2_stage_pitch(npt, 4);  // >= either T's pitch
-  size_t xb = (size_t)tsize * N * (N | 1), sb = (size_t)8 * 2 * P2_KC * spd;
+  const int npt = (N + 3) & ~3;
+  const int spd = p2_stage_pitch(npt, 8) > p2_stage_pitch(npt, 4) ? p2_stage_pitch(npt, 8) : p2_stage_pitch(npt, 4);
+  size_t xb = (size_t)tsize * N * (N | 1), sb = (size_t)8 * P2_NS * P2_KC * spd;
   const size_t kb = 8 * (size_t)N * (N <= 32 ? 33 : 65);  // key rows (pitch 32 KB + 1)
   if (kb > xb) xb = kb;
   for (int q = 0; q < 2; q++) {
     s.x[q] = take(xb > sb ? xb : sb);  // X_K (aliases the u/v staging while it is built)
-    s.ord[q] = take((size_t)N * p2_ord_pitch(N));  // row orders (columns, value desc / column asc)
+    s.ord[q] = take((size_t)N * N);    // row orders (columns, value desc / column asc)
   }
   s.meta = take(2 * sizeof(P2Meta));
   s.red = take(8 * sizeof(double));  // one partial per producer warp
   s.amb = take(((kcap >> 5) + 1) * sizeof(uint32_t));
   s.item = take(sizeof(int64_t));
   s.first = take(sizeof(int32_t) * 4);  // first stop, emin, emax
+  s.mrow = take(sizeof(int32_t) * 128);  // the consumer's winners: column (value path) / key hi, lo
   s.tab = take(sizeof(double) * (kcap + 2));  // alpha^m
   s.total = o;
   return s;
@@ -491,39 +478,23 @@ __device__ __forceinline__ void p2_sort_row(const T *row, int N, uint8_t *ord, i
   }
 }
 
-// W = Python's left-to-right sum (similarity.py:150) of the matched values of
-// rows 0..N-1, lane l holding rows l + 32 cc: the values are broadcast in row
-// order, every lane ends with the same sum (the dependent adds overlap the
-// shuffles instead of a lane-0 loop over shared memory)
-template <int KB>
-__device__ __forceinline__ double p2_row_sum(const double (&v)[KB], int N) {
-  double w = 0.0;
-#pragma unroll
-  for (int cc = 0; cc < KB; cc++)
-    for (int l = 0; l < 32 && l + 32 * cc < N; l++) w += __shfl_sync(0xffffffffu, v[cc], l);
-  return w;
-}
-
 // Greedy rounds (similarity.py:96-108) on sorted rows, one warp: each round
 // takes the best current head over active rows (ties -> lowest row) and
-// advances the rows whose head column was taken.  Returns W (:150), the
-// row-order sum (every lane).
+// advances the rows whose head column was taken.  Returns W (:150) on lane 0
+// (row-order sum), mrow[i] = matched column.
 template <typename T, int KB>
-__device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uint8_t *ord, int lane) {
-  const int OP = p2_ord_pitch(N);
+__device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uint8_t *ord, int32_t *mrow, int lane) {
   int ptr[KB], ccol[KB];
   T cur[KB];
   bool act[KB];
   uint32_t taken[KB];
-  double win[KB];  // matched value of the lane's rows
 #pragma unroll
   for (int cc = 0; cc < KB; cc++) {
     const int i = lane + 32 * cc;
     act[cc] = i < N;
     ptr[cc] = 0;
     taken[cc] = 0u;
-    win[cc] = 0.0;
-    ccol[cc] = act[cc] ? (int)ord[i * OP] : 0;
+    ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
     cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
   }
   for (int round = 0; round < N; round++) {
@@ -542,12 +513,10 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
     for (int cc = 0; cc < KB; cc++)
       if (cc == (brow >> 5)) mycol = ccol[cc];
     const int bcol = __shfl_sync(0xffffffffu, mycol, brow & 31);
+    if (lane == 0) mrow[brow] = bcol;
 #pragma unroll
     for (int cc = 0; cc < KB; cc++) {
-      if (lane + 32 * cc == brow) {
-        act[cc] = false;
-        win[cc] = (double)cur[cc];
-      }
+      if (lane + 32 * cc == brow) act[cc] = false;
       if (cc == (bcol >> 5)) taken[cc] |= 1u << (bcol & 31);
     }
 #pragma unroll
@@ -558,7 +527,7 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
         bool tk;
         do {
           ++p;
-          col = ord[i * OP + p];
+          col = ord[i * N + p];
           uint32_t word = 0;
 #pragma unroll
           for (int q = 0; q < KB; q++)
@@ -571,7 +540,11 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
       }
     }
   }
-  return p2_row_sum<KB>(win, N);
+  __syncwarp();
+  double wsum = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < N; i++) wsum += (double)Xs[i * P + mrow[i]];
+  return wsum;
 }
 
 // ---- exact packed keys: (value bits | 6-bit column field), comparable across
@@ -733,24 +706,21 @@ __device__ __forceinline__ void p2_row_order_pair(const unsigned long long *Krow
 // Greedy rounds on sorted key rows (pitch PK), one warp: a head's cross-row
 // key swaps the column field for (63 - row), so one 64-bit max picks the best
 // head with ties to the lowest row — np.argmax's first occurrence.
-#ifdef CFGSIM_P2_NOPREFETCH
 template <typename T, int KB>
 __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, const uint8_t *ord, int N, int emin,
-                                                 int lane) {
-  const int OP = p2_ord_pitch(N);
+                                                 int32_t *mrow, int lane) {
   unsigned long long hk[KB];
   int ptr[KB];
   bool act[KB];
   unsigned long long taken = 0ull;
-  unsigned long long win[KB];
 #pragma unroll
   for (int cc = 0; cc < KB; cc++) {
     const int i = lane + 32 * cc;
     act[cc] = i < N;
     ptr[cc] = 0;
-    win[cc] = 0ull;
-    hk[cc] = act[cc] ? Kr[i * PK + ord[i * OP]] : 0ull;
+    hk[cc] = act[cc] ? Kr[i * PK + ord[i * N]] : 0ull;
   }
+  double wsum = 0.0;
   for (int round = 0; round < N; round++) {
     unsigned long long g = 0ull;
 #pragma unroll
@@ -767,104 +737,34 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
       if ((brow >> 5) == cc) mine = hk[cc];
     const unsigned long long wk = __shfl_sync(0xffffffffu, mine, brow & 31);
     const int bcol = 63 - (int)(wk & 63ull);
+    if (lane == 0) {
+      mrow[2 * brow] = (int)(unsigned)(wk >> 32);  // winning key (value bits) for W
+      mrow[2 * brow + 1] = (int)(unsigned)wk;
+    }
     taken |= 1ull << bcol;
 #pragma unroll
     for (int cc = 0; cc < KB; cc++) {
-      if (lane + 32 * cc == brow) {
-        act[cc] = false;
-        win[cc] = hk[cc];
-      }
+      if (lane + 32 * cc == brow) act[cc] = false;
       if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
         const int i = lane + 32 * cc;
         int p = ptr[cc], col;
         do {
           ++p;
-          col = ord[i * OP + p];
+          col = ord[i * N + p];
         } while ((taken >> col) & 1ull);
         ptr[cc] = p;
         hk[cc] = Kr[i * PK + col];
       }
     }
   }
-  double v[KB];
-#pragma unroll
-  for (int cc = 0; cc < KB; cc++) v[cc] = lane + 32 * cc < N ? p2_key_value<T>(win[cc], emin) : 0.0;
-  return p2_row_sum<KB>(v, N);  // similarity.py:150: Python's sum, row order
-}
-#else
-template <typename T, int KB>
-__device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, int PK, const uint8_t *ord, int N, int emin,
-                                                 int lane) {
-  const int OP = p2_ord_pitch(N);
-  // per row: head key hk (position ptr) and the next position's column nc
-  // and key nk, loaded one advance ahead, so the common advance by one
-  // position (the next column is free) has no shared-memory load on the
-  // round's critical path
-  unsigned long long hk[KB], nk[KB];
-  int ptr[KB], nc[KB];
-  bool act[KB];
-  unsigned long long taken = 0ull;
-  unsigned long long win[KB];  // winning key of the lane's rows
-#pragma unroll
-  for (int cc = 0; cc < KB; cc++) {
-    const int i = lane + 32 * cc;
-    act[cc] = i < N;
-    ptr[cc] = 0;
-    win[cc] = 0ull;
-    hk[cc] = act[cc] ? Kr[i * PK + ord[i * OP]] : 0ull;
-    nc[cc] = (act[cc] && N > 1) ? (int)ord[i * OP + 1] : 0;
-    nk[cc] = (act[cc] && N > 1) ? Kr[i * PK + nc[cc]] : 0ull;
-  }
-  for (int round = 0; round < N; round++) {
-    unsigned long long g = 0ull;
-#pragma unroll
-    for (int cc = 0; cc < KB; cc++) {
-      const unsigned long long gk = (hk[cc] & ~63ull) | (unsigned long long)(63 - (lane + 32 * cc));
-      if (act[cc] && gk > g) g = gk;
+  __syncwarp();
+  if (lane == 0)  // similarity.py:150: Python's sum, row order
+    for (int i = 0; i < N; i++) {
+      const unsigned long long k = ((unsigned long long)(unsigned)mrow[2 * i] << 32) | (unsigned)mrow[2 * i + 1];
+      wsum += p2_key_value<T>(k, emin);
     }
-    const unsigned ghi = __reduce_max_sync(0xffffffffu, (unsigned)(g >> 32));
-    const unsigned glo = __reduce_max_sync(0xffffffffu, (unsigned)(g >> 32) == ghi ? (unsigned)g : 0u);
-    const int brow = 63 - (int)(glo & 63u);
-    unsigned long long mine = hk[0];
-#pragma unroll
-    for (int cc = 1; cc < KB; cc++)
-      if ((brow >> 5) == cc) mine = hk[cc];
-    const unsigned long long wk = __shfl_sync(0xffffffffu, mine, brow & 31);
-    const int bcol = 63 - (int)(wk & 63ull);
-    taken |= 1ull << bcol;
-#pragma unroll
-    for (int cc = 0; cc < KB; cc++) {
-      if (lane + 32 * cc == brow) {
-        act[cc] = false;
-        win[cc] = hk[cc];
-      }
-      if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
-        const int i = lane + 32 * cc;
-        int p = ptr[cc] + 1;  // an active row always has an untaken column ahead
-        if ((taken >> nc[cc]) & 1ull) {
-          int col;
-          do {
-            ++p;
-            col = ord[i * OP + p];
-          } while ((taken >> col) & 1ull);
-          hk[cc] = Kr[i * PK + col];
-        } else {
-          hk[cc] = nk[cc];
-        }
-        ptr[cc] = p;
-        if (p + 1 < N) {  // next position, consumed at this row's next advance
-          nc[cc] = ord[i * OP + p + 1];
-          nk[cc] = Kr[i * PK + nc[cc]];
-        }
-      }
-    }
-  }
-  double v[KB];
-#pragma unroll
-  for (int cc = 0; cc < KB; cc++) v[cc] = lane + 32 * cc < N ? p2_key_value<T>(win[cc], emin) : 0.0;
-  return p2_row_sum<KB>(v, N);  // similarity.py:150: Python's sum, row order
+  return wsum;
 }
-#endif
 
 template <typename T, int KB, int AR, int BC, int PW, int MINB>
 __global__ void __launch_bounds__(32 * (PW + 1), MINB)
@@ -888,6 +788,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   if (warp == PW) {
     // ---------------- consumer: greedy rounds of the pairs in order
     // (a second consumer warp owning one buffer each measured 2% slower)
+    int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
     unsigned long long ph_t = 0;
     int ph_last = -1;
     for (int it = 0;; it++) {
@@ -900,8 +801,8 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       const T *Xs = (const T *)(smem_raw + L.x[s]);
       const double wsum =
           mt.keys ? p2_rounds_keys<T, KB>((const unsigned long long *)Xs, 32 * KB + 1, smem_raw + L.ord[s], N, mt.emin,
-                                          lane)
-                  : p2_rounds<T, KB>(Xs, P, N, smem_raw + L.ord[s], lane);
+                                          mrow, lane)
+                  : p2_rounds<T, KB>(Xs, P, N, smem_raw + L.ord[s], mrow, lane);
       if (lane == 0) {
         if (out.d) out.d[mt.slot] = isorank_distance_of(wsum, N);
         if (out.W) out.W[mt.slot] = wsum;
@@ -1049,17 +950,21 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
     const int sstep = NP / w2, sq = tid % w2, smm0 = tid / w2;
     const int sside = sq >= upr, sr = (sq - sside * upr) * EPU;
     const T *ssrc = (sside ? UB : UA) + sr;
+    // a P2_NS-deep ring: chunk ch lives in buffer ch % P2_NS; two chunks
+    // are in flight while one is multiplied, one producer barrier per chunk
     auto stage = [&](int ch) {
-      T *dst = stg + (ch & 1) * P2_KC * SPD + sside * NPt + sr;
-      const int m0 = ch * P2_KC;
-      if (smm0 < sstep)
+      if (ch < nch && smm0 < sstep) {
+        T *dst = stg + (ch % P2_NS) * P2_KC * SPD + sside * NPt + sr;
+        const int m0 = ch * P2_KC;
         for (int mm = smm0; mm < P2_KC; mm += sstep) {
           const bool ok = m0 + mm <= K;
           big_cp_async_zfill<16>(dst + mm * SPD, ssrc + (size_t)(ok ? m0 + mm : 0) * NPt, ok);
         }
-      big_cp_async_commit();
+      }
+      big_cp_async_commit();  // (empty groups past the last chunk keep the wait counts uniform)
     };
-    stage(0);
+#pragma unroll
+    for (int q = 0; q + 1 < P2_NS; q++) stage(q);
     int emn = 0x7fffffff, emx = -1;
     int emin = 0;
     bool keys = true;
@@ -1080,14 +985,10 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
 #pragma unroll
         for (int y = 0; y < TC; y++) acc[x][y][0] = acc[x][y][1] = 0.0;
       for (int ch = 0; ch < nch; ch++) {
-        if (ch + 1 < nch) {
-          stage(ch + 1);
-          big_cp_async_wait_group<1>();
-        } else {
-          big_cp_async_wait_group<0>();
-        }
-        nbar_sync(BAR_P, NP);
-        const T *buf = stg + (ch & 1) * P2_KC * SPD;  // (fp32 mode: rows promoted to fp64 for the mma)
+        big_cp_async_wait_group<P2_NS - 2>();  // this thread's copies of chunk ch have landed
+        nbar_sync(BAR_P, NP);                  // everyone's have; everyone is done with chunk ch - 1
+        stage(ch + P2_NS - 1);                 // into chunk ch - 1's buffer
+        const T *buf = stg + (ch % P2_NS) * P2_KC * SPD;  // (fp32 mode: rows promoted to fp64 for the mma)
         const int m0 = ch * P2_KC;
 #pragma unroll
         for (int k0 = 0; k0 < P2_KC; k0 += 4) {
@@ -1115,8 +1016,9 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
                            : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
                            : "d"(af[x]), "d"(bf[y]));
         }
-        nbar_sync(BAR_P, NP);  // buffer (ch & 1) is re-staged by chunk ch + 2 / keys overwrite it
       }
+      big_cp_async_wait_group<0>();  // (only empty groups remain; the producer barrier below the
+                                     // exponent reduction orders the key writes after every read)
 #pragma unroll
       for (int x = 0; x < TR; x++)
 #pragma unroll
@@ -1161,12 +1063,12 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       if constexpr (KB == 2) {  // two adjacent lanes per row
         const int row = tid >> 1, half = tid & 1;
         const bool act = row < N;
-        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * p2_ord_pitch(N), half, act);
+        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * N, half, act);
       } else {
-        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * p2_ord_pitch(N));
+        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * N);
       }
     } else {
-      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * p2_ord_pitch(N), lane);
+      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * N, lane);
     }
     if (tid == 0) {
       meta[s].slot = slot;

@@ -152,6 +152,21 @@ def nearest_sharded(n_corpus: int, compute_shard: Callable[[int, int], tuple], *
     return best.cpu().numpy(), idx.cpu().numpy()
 
 
+def _all_gather(dst, src, group=None):
+    """``all_gather_into_tensor`` on the group's backend: NCCL gathers device
+    tensors over NVLink in place; gloo (the CPU multi-process tests, and
+    several ranks sharing one GPU) gathers host copies."""
+    import torch.distributed as dist
+
+    if src.is_cuda and dist.get_backend(group) == "gloo":
+        import torch
+        g = torch.empty(dst.shape, dtype=dst.dtype)
+        dist.all_gather_into_tensor(g, src.cpu(), group=group)
+        dst.copy_(g)
+    else:
+        dist.all_gather_into_tensor(dst, src, group=group)
+
+
 def _world(group):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
@@ -197,7 +212,7 @@ def pairwise_sharded(matrices, *, alpha: float = 0.85, tol: float = 1e-9, max_it
             nat.check(nat.lib.cfgsim_allpairs_range(C.handle, u0, u1, 0, nat.C.byref(prm), nat.ptr(d_lin), None, st))
         if world > 1:
             gathered = torch.empty(world * chunk, dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(gathered, d_lin, group=group)
+            _all_gather(gathered, d_lin, group)
             full = torch.cat([gathered[r * chunk:r * chunk + int(bounds[r + 1] - bounds[r])] for r in range(world)])
         else:
             full = d_lin[: u1 - u0]
@@ -237,7 +252,7 @@ def nearest_gpu_sharded(queries, corpus, *, alpha: float = 0.85, tol: float = 1e
         if world > 1:
             gd = torch.empty(world * nq, dtype=torch.float64, device=dev)
             gi = torch.empty(world * nq, dtype=torch.int64, device=dev)
-            dist.all_gather_into_tensor(gd, bd, group=group)
-            dist.all_gather_into_tensor(gi, bi, group=group)
+            _all_gather(gd, bd, group)
+            _all_gather(gi, bi, group)
             bd, bi = merge_best(gd.view(world, nq), gi.view(world, nq))
         return bd.cpu().numpy(), bi.cpu().numpy()

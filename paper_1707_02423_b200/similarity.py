@@ -214,6 +214,45 @@ def pairwise(matrices: list[TransitionMatrix], measure: MeasureId, *, p: float =
     return (pm, iters) if return_iterations else pm
 
 
+def pairwise_all(matrices: list[TransitionMatrix], measures=None, *, p: float = 3.0, alpha: float = 0.85,
+                 tol: float = 1e-9, max_iter: int = 1000, precision: str = "fp64", symmetric: bool = True,
+                 device: int | None = None) -> dict:
+    """``pairwise`` for several measures at once — what ``sasscfg compare
+    --measure all`` computes (cli.py:150-165: one ``pairwise`` per measure).
+    Returns {MeasureId: PairwiseMatrix}, each equal to ``pairwise(matrices,
+    measure, ...)``.  The corpus is packed and uploaded once; the five flat
+    measures come from ONE kernel pass over each pair's size-normalised
+    entries (``cfgsim_flat_all_allpairs``) instead of five; ISO runs the
+    IsoRank kernels on the same device corpus."""
+    if measures is None:
+        measures = tuple(MeasureId)
+    measures = tuple(MeasureId(m) for m in measures)
+    if len(matrices) < 2:
+        raise ValueError("pairwise comparison needs at least 2 kernels")
+    ordered = sorted(matrices, key=lambda m: m.kernel_id)
+    ids = tuple(m.kernel_id for m in ordered)
+    if len(set(ids)) != len(ids):
+        raise DuplicateKernel("duplicate kernel_id in pairwise input")
+    k = len(ordered)
+    out = {}
+    flat = [m for m in measures if m is not MeasureId.ISO]
+    with DeviceCorpus(ordered, _dev(device)) as corpus:
+        if flat:
+            mats5 = np.empty((5, k, k))
+            nat.check(nat.lib.cfgsim_flat_all_allpairs(corpus.handle, float(p), nat.ptr(mats5), None))
+            for m in flat:
+                out[m] = PairwiseMatrix(measure=m, kernel_ids=ids, scores=mats5[nat.FLAT_IDS[m.value]].copy(),
+                                        scaled=False)
+        if MeasureId.ISO in measures:
+            _check_alpha(alpha)
+            scores = np.empty((k, k))
+            prm = nat.params(alpha, tol, max_iter, precision)
+            nat.check(nat.lib.cfgsim_allpairs(corpus.handle, 0 if symmetric else 1, nat.C.byref(prm),
+                                              nat.ptr(scores), None, None))
+            out[MeasureId.ISO] = PairwiseMatrix(measure=MeasureId.ISO, kernel_ids=ids, scores=scores, scaled=False)
+    return {m: out[m] for m in measures}
+
+
 def minmax_scale(pm: PairwiseMatrix) -> PairwiseMatrix:
     """Affine rescale to [0, 1] over finite entries (``similarity.py:260-284``);
     ISO's diagonal takes part, the flat measures' zero diagonal does not."""

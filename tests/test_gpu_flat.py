@@ -103,3 +103,30 @@ def test_flat_pairwise_nan_and_large(P):
             assert pe.scores[i, j] == pytest.approx(np.sqrt(np.sum((x - y) ** 2)), rel=1e-12)
     pn = P.pairwise(tms, P.MeasureId.MIN, p=0.5)
     assert np.isnan(pn.scores[~np.eye(len(ms), dtype=bool)]).all()
+
+
+@pytest.mark.parametrize("p", [3.0, 1.5, 0.5])
+def test_pairwise_all_one_pass_equals_per_measure(P, p):
+    """`compare --measure all` (cli.py:150-165) through pairwise_all: the five
+    flat matrices from one kernel pass are bitwise the per-measure pairwise()
+    outputs (same sums, same order), ISO equals pairwise(ISO); the bundled
+    corpus also matches the reference's own matrices (p = 3)."""
+    from paper_1707_02423_b200 import synth
+    g = load_golden("bundled_corpus.npz")
+    mats = unravel(g["sizes"], g["flat"]) + synth.random_corpus(30, 3, 90, seed=4)
+    tms = [P.TransitionMatrix(f"k{i:03d}.a.b", m, tuple(range(len(m))), P.ROW_STOCHASTIC) for i, m in enumerate(mats)]
+    allm = P.pairwise_all(tms, p=p)
+    assert list(allm) == list(P.MeasureId)
+    for m, pm in allm.items():
+        ref = P.pairwise(tms, m, p=p)
+        assert pm.kernel_ids == ref.kernel_ids and pm.measure is m
+        np.testing.assert_array_equal(pm.scores, ref.scores)
+    if p == 3.0:
+        f = load_golden("flat.npz")
+        six = P.pairwise_all(tms[:len(g["ids"])], measures=["euc", "man", "min", "jac", "cos"])
+        for mid in ("euc", "man", "min", "jac", "cos"):
+            tm = [P.TransitionMatrix(str(k), m, tuple(range(len(m))), P.ROW_STOCHASTIC)
+                  for k, m in zip(g["ids"], unravel(g["sizes"], g["flat"]))]
+            np.testing.assert_allclose(P.pairwise_all(tm, measures=[mid])[P.MeasureId(mid)].scores,
+                                       f[f"bundled_{mid}"], rtol=1e-12, atol=1e-14)
+        assert len(six) == 5

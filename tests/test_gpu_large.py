@@ -169,3 +169,30 @@ def test_reference_mid_size_pair(P):
         d, w, it, cv = P.isorank_pairs(C, C, [0], [1])
     assert it[0] == int(R["iterations"]) and cv[0]
     assert d[0] == pytest.approx(float(R["d"]), rel=RTOL64)
+
+
+@pytest.mark.parametrize("na,nb,seed", [(150, 200, 1), (520, 520, 2), (700, 333, 3)])
+def test_start_vector_beyond_on_chip_tiers(P, na, nb, seed):
+    """isorank_align(start=...) for N > 128 (similarity.py:135, pinned by
+    pkg/tests/test_similarity.py:183-189 at small N): the reference iteration
+    with X in HBM (csrc/isorank_start.cuh) against the numpy restatement —
+    identical iterations and convergence, X to 1e-10, W and d to 1e-9."""
+    from oracle import isorank_np as O
+    from paper_1707_02423_b200 import synth
+    rng = np.random.default_rng(seed)
+    a = synth.random_corpus(1, na, na, seed=seed)[0]
+    b = synth.random_corpus(1, nb, nb, seed=seed + 100)[0]
+    ta = P.TransitionMatrix("a.s.x", a, tuple(range(na)), P.ROW_STOCHASTIC)
+    tb = P.TransitionMatrix("b.s.x", b, tuple(range(nb)), P.ROW_STOCHASTIC)
+    ta, tb = P.normalize_pair(ta, tb)
+    N = ta.n
+    start = rng.random(N * N) + 0.05
+    al = P.isorank_align(ta, tb, start=start)
+    Xo, mo, wo, ito, cvo = O.isorank_align(np.asarray(ta.entries), np.asarray(tb.entries), start=start)
+    assert al.iterations == ito and al.converged == cvo
+    np.testing.assert_allclose(al.matrix, Xo, rtol=1e-10)
+    assert abs(al.matched_weight - wo) <= RTOL64 * abs(wo)
+    assert sorted(al.matching) == list(range(N))
+    assert_greedy_equivalent(Xo, al.matching)
+    d = P.isorank_distance(al)
+    assert abs(d - O.isorank_distance_from(wo, N)) <= RTOL64 * d
