@@ -28,6 +28,7 @@
 #include "flat.cuh"
 #include "ward.cuh"
 #include "isorank_start.cuh"
+#include "cost_model.h"
 
 using namespace cfgsim;
 
@@ -259,6 +260,7 @@ struct Scratch {
   int64_t ovf_cap = 0;
   DBuf pool_lin, pool_it, pool_out[4];  // per-call outputs, grow-only (no cudaMalloc/cudaFree per call)
   PinBuf pin_out[4], pin_in;            // pinned staging of host outputs / corpus uploads
+  cudaStream_t copy_stream = nullptr;   // D2H of pipelined all-pairs chunks
   std::recursive_mutex mu;
   cudaEvent_t done = nullptr;  // recorded at the end of the last call's stream work
   int depth = 0;               // nesting of guards on the owning thread
@@ -375,6 +377,18 @@ bool use_lowrank() {
 }
 
 bool lr_supported(int precision, int N) { return N <= lr_tiers(precision).back().nmax; }
+// Pairs with N above this go to the large-N kernel even where a low-rank tier
+// exists: measured per-unit cost (tools/calibrate_split.py) low-rank 2.39 /
+// 2.89 / 3.16 us at N = 96 / 112 / 128 vs large-N 2.35 us at N = 129.
+// CFGSIM_BIG_MIN overrides (A/B).
+int big_min() {
+  static const int v = [] {
+    const char *e = getenv("CFGSIM_BIG_MIN");
+    return e ? atoi(e) : 96;
+  }();
+  return v;
+}
+bool lr_tier(int precision, int N) { return lr_supported(precision, N) && N <= big_min(); }
 
 int lr_launch(int precision, int nlim, bool dense_lists, const DevCorpus &A, const DevCorpus &B,
               const PairWork &work, const PairOut &out, const cfgsim_params *p, unsigned long long *counter,
@@ -530,7 +544,7 @@ int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, 
     double tot = 0;
     for (int k = 0; k < 5; k++) tot += (double)ph[k];
     fprintf(stderr, "[cfgsim big N<=%d] phase cycles (sum over CTAs): operators %.1f%% sweeps %.1f%% gemm %.1f%% "
-            "sort %.1f%% greedy %.1f%% total %.3e | sum N %llu proposals %llu (unused %llu)\n", nlim, 100 * ph[0] / tot,
+            "sort %.1f%% greedy %.1f%% total %.3e | sum N %llu advances %llu deep %llu\n", nlim, 100 * ph[0] / tot,
             100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot, tot, ph[7], ph[5], ph[6]);
   }
   return CFGSIM_OK;
@@ -1028,7 +1042,7 @@ int run_list(const cfgsim_corpus *A, const cfgsim_corpus *B, const std::vector<i
     const int N = std::max(A->n_nodes[ia[q]], B->n_nodes[ib[q]]);
     Plan pl;
     if (lr) {
-      if (lr_supported(p->precision, N)) {
+      if (lr_tier(p->precision, N)) {
         pl.ti = N;  // bucket key: one low-rank launch per exact N
       } else if (N <= kBigNmax) {
         pl.ti = kBigKey + big_kb(N);  // large-N kernel, one launch per sort class
@@ -1565,16 +1579,16 @@ int cfgsim_allpairs_units(const cfgsim_corpus *c, int64_t *n_units) {
 
 int cfgsim_allpairs_split(const cfgsim_corpus *c, int32_t world, int64_t *bounds) {
   if (!c || world < 1 || !bounds) return fail(CFGSIM_ERR_ARG, "bad arguments");
-  // cost of unit (a, b>=a) ~ N^2 with N = n_sorted[a] (rows sorted by n desc)
+  // cost of unit (a, b >= a) = unit_cost_us(N), N = n_sorted[a] (rows sorted
+  // by n desc): the measured per-tier cost model of cost_model.h
   std::vector<double> cum(c->K + 1, 0.0);
-  for (int a = 0; a < c->K; a++)
-    cum[a + 1] = cum[a] + (double)(c->K - a) * (double)c->n_sorted[a] * c->n_sorted[a];
+  for (int a = 0; a < c->K; a++) cum[a + 1] = cum[a] + (double)(c->K - a) * unit_cost_us(c->n_sorted[a]);
   const double total = cum[c->K];
   bounds[0] = 0;
   for (int r = 1; r < world; r++) {
     const double target = total * r / world;
     const int a = (int)(std::upper_bound(cum.begin(), cum.end(), target) - cum.begin()) - 1;
-    const double per = (double)c->n_sorted[std::min(a, c->K - 1)] * c->n_sorted[std::min(a, c->K - 1)];
+    const double per = unit_cost_us(c->n_sorted[std::min(a, c->K - 1)]);
     int64_t u = c->row_start[a] + (int64_t)std::ceil((target - cum[a]) / per);
     u = std::min<int64_t>(u, c->row_start[std::min(a + 1, c->K)]);
     bounds[r] = std::max(u, bounds[r - 1]);
@@ -1635,10 +1649,10 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
     const int N = c->n_sorted[a];
     int a_end = a;
     Plan pl;
-    const bool big = lr && !lr_supported(p->precision, N);
+    const bool big = lr && !lr_tier(p->precision, N);
     if (big) {
       if (N > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
-      while (a_end + 1 < c->K && !lr_supported(p->precision, c->n_sorted[a_end + 1]) &&
+      while (a_end + 1 < c->K && !lr_tier(p->precision, c->n_sorted[a_end + 1]) &&
              big_kb(c->n_sorted[a_end + 1]) == big_kb(N))
         a_end++;
     } else if (lr) {
@@ -1694,6 +1708,89 @@ int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const doubl
   return CFGSIM_OK;
 }
 
+// Host-output all-pairs as a pipeline: the unit triangle in cost-balanced
+// chunks; chunk j's unit-linear results go to pinned host memory on a copy
+// stream as soon as its kernels finish, and host threads scatter them into
+// the caller's K x K matrices (both triangles, caller's graph order) while
+// the GPU computes chunk j + 1.  Only the last chunk's copy and scatter are
+// exposed after the kernels (the one-shot path: device scatter, 32 MB D2H of
+// the full matrix and a host copy, all after the last kernel).
+int allpairs_host_pipelined(const cfgsim_corpus *c, const cfgsim_params *p, double *d_mat, int32_t *iters_mat,
+                            cudaStream_t st) {
+  const int64_t nu = c->row_start[c->K];
+  const int K = c->K;
+  Scratch &S = scratch_for(c->device);
+  CU(grow_buf(S.pool_lin, sizeof(double) * nu, st));
+  if (iters_mat) CU(grow_buf(S.pool_it, sizeof(int32_t) * nu, st));
+  CU(S.pin_out[0].grow(sizeof(double) * nu));
+  if (iters_mat) CU(S.pin_out[1].grow(sizeof(int32_t) * nu));
+  double *dl = S.pool_lin.as<double>();
+  int32_t *il = iters_mat ? S.pool_it.as<int32_t>() : nullptr;
+  double *hd = (double *)S.pin_out[0].p;
+  int32_t *hi = iters_mat ? (int32_t *)S.pin_out[1].p : nullptr;
+  const int nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(6, nu / 20000));
+  std::vector<int64_t> b(nchunk + 1);
+  if (int rc = cfgsim_allpairs_split(c, nchunk, b.data())) return rc;
+  if (!S.copy_stream) CU(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> done(nchunk, nullptr), copied(nchunk, nullptr);
+  auto cleanup = [&] {
+    for (auto e : done) if (e) cudaEventDestroy(e);
+    for (auto e : copied) if (e) cudaEventDestroy(e);
+  };
+  for (int j = 0; j < nchunk; j++) {
+    CU(cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&copied[j], cudaEventDisableTiming));
+  }
+  for (int j = 0; j < nchunk; j++) {
+    const int64_t u0 = b[j], u1 = b[j + 1];
+    if (u1 > u0) {
+      if (int rc = cfgsim_allpairs_range(c, u0, u1, 0, p, dl + u0, il ? il + u0 : nullptr, st)) {
+        cleanup();
+        return rc;
+      }
+    }
+    CU(cudaEventRecord(done[j], st));
+    CU(cudaStreamWaitEvent(S.copy_stream, done[j], 0));
+    if (u1 > u0) {
+      CU(cudaMemcpyAsync(hd + u0, dl + u0, sizeof(double) * (u1 - u0), cudaMemcpyDeviceToHost, S.copy_stream));
+      if (hi) CU(cudaMemcpyAsync(hi + u0, il + u0, sizeof(int32_t) * (u1 - u0), cudaMemcpyDeviceToHost, S.copy_stream));
+    }
+    CU(cudaEventRecord(copied[j], S.copy_stream));
+  }
+  // host scatter of each chunk as it lands (unit u -> sorted rows a <= b;
+  // the matrix entries (perm[a], perm[b]) and (perm[b], perm[a]))
+  const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const auto &rs = c->row_start;
+  const auto &perm = c->perm;
+  for (int j = 0; j < nchunk; j++) {
+    CU(cudaEventSynchronize(copied[j]));
+    const int64_t u0 = b[j], u1 = b[j + 1];
+    const int64_t per = (u1 - u0 + nt - 1) / nt;
+    auto work = [&](int t) {
+      const int64_t s0 = u0 + per * t, s1 = std::min(u1, s0 + per);
+      if (s0 >= s1) return;
+      int64_t a = (int64_t)(std::upper_bound(rs.begin(), rs.end(), s0) - rs.begin()) - 1;
+      for (int64_t u = s0; u < s1; u++) {
+        while (rs[a + 1] <= u) a++;
+        const int64_t bb = a + (u - rs[a]);
+        const size_t x = (size_t)perm[a], y = (size_t)perm[bb];
+        d_mat[x * K + y] = hd[u];
+        d_mat[y * K + x] = hd[u];
+        if (iters_mat) {
+          iters_mat[x * K + y] = hi[u];
+          iters_mat[y * K + x] = hi[u];
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; t++) pool.emplace_back(work, t);
+    work(0);
+    for (auto &th : pool) th.join();
+  }
+  cleanup();
+  return CFGSIM_OK;
+}
+
 int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params *p,
                     double *d_mat, int32_t *iters_mat, void *cuda_stream) {
   CFGSIM_NVTX("cfgsim.allpairs");
@@ -1702,6 +1799,15 @@ int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params
   if (int rc = set_device(c->device)) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   DeviceGuard guard(c->device, st);
+  static const bool pipelined = [] {  // CFGSIM_PIPELINE=0: the one-shot path (A/B)
+    const char *e = getenv("CFGSIM_PIPELINE");
+    return !(e && std::string(e) == "0");
+  }();
+  if (pipelined && !ordered && !is_device_ptr(d_mat) && (!iters_mat || !is_device_ptr(iters_mat))) {
+    int rc = allpairs_host_pipelined(c, p, d_mat, iters_mat, st);
+    if (rc == CFGSIM_OK) CU(cudaStreamSynchronize(st));
+    return rc;
+  }
   const int64_t nu = c->row_start[c->K];
   const int64_t slots = ordered ? 2 * nu : nu;
   Scratch &S = scratch_for(c->device);
@@ -1934,7 +2040,7 @@ int cfgsim_nearest(const cfgsim_corpus *Q, const cfgsim_corpus *C, int32_t c0, i
     for (int N : ns) {
       if (two && N <= kSeqNmax) continue;
       if (N > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(N) + " exceeds 1024");
-      const int key = (!lr || lr_supported(p->precision, N)) ? N : kBigKey + big_kb(N);
+      const int key = (!lr || lr_tier(p->precision, N)) ? N : kBigKey + big_kb(N);
       if (launches.empty() || launches.back().key != key) launches.push_back({key, N, {}});
       Launch &L = launches.back();
       L.nlim = std::max(L.nlim, N);

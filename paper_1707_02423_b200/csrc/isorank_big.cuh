@@ -782,6 +782,36 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           key[c] = k;
         }
         big_sort_desc<uint32_t, KB>(key, lane);
+        // The 32-bit order is exact except where neighbours share a 22-bit
+        // prefix but differ in value (exactly equal values are already in
+        // column order: the key's low bits).  Typically no row has such a
+        // pair — then the order is final; else the repair below.
+        auto kcol = [&](uint32_t k) { return (1 << BIG_CB) - 1 - (int)(k & ((1u << BIG_CB) - 1)); };
+        bool need = false;
+#pragma unroll
+        for (int c = 0; c + 1 < KB; c++)
+          if (lane * KB + c + 1 < N && (key[c] >> BIG_CB) == (key[c + 1] >> BIG_CB))
+            need = need || row[big_rpos(kcol(key[c]))] != row[big_rpos(kcol(key[c + 1]))];
+        {
+          const uint32_t nk = __shfl_down_sync(0xffffffffu, key[0], 1);
+          if (lane < 31 && lane * KB + KB < N && (key[KB - 1] >> BIG_CB) == (nk >> BIG_CB))
+            need = need || row[big_rpos(kcol(key[KB - 1]))] != row[big_rpos(kcol(nk))];
+        }
+        if (!__any_sync(0xffffffffu, need)) {
+          unsigned long long *ov = sval + (size_t)i * N;
+          uint16_t *oc = scol + (size_t)i * N;
+#pragma unroll
+          for (int c = 0; c < KB; c++) {
+            const int pos = lane * KB + c;
+            if (pos < N) {
+              const int col = kcol(key[c]);
+              ov[pos] = big_bits(row[big_rpos(col)]);  // exact value bits for the matching
+              oc[pos] = (uint16_t)col;
+            }
+          }
+          __syncwarp();  // rbuf is restaged for the warp's next row
+          continue;
+        }
         // pair-wide 64-bit keys (exponent | mantissa truncated by `shift` bits |
         // column) in sorted order; odd-even transposition repairs inversions
         // among equal 22-bit prefixes, then neighbours whose truncated keys
@@ -849,13 +879,16 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       // so no HBM round trip sits on the per-round critical path.
       {
         uint32_t *taken = (uint32_t *)(smem_raw + L.taken);
-        unsigned long long *slot_v = (unsigned long long *)(smem_raw + L.gslot);
-        int32_t *slot_r = (int32_t *)(slot_v + 2 * BIG_WARPS);
-        int32_t *slot_c = slot_r + 2 * BIG_WARPS;
+        // per warp and round parity: {value bits, row << 32 | column} (one
+        // 16-byte load per slot in the scan)
+        ulonglong2 *gsl = (ulonglong2 *)(smem_raw + L.gslot);
         int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
         unsigned long long *mval = (unsigned long long *)(smem_raw + L.mval);
         for (int w = tid; w < 64; w += NT) taken[w] = 0u;
-        constexpr int PF = 3;  // prefetch depth (positions ahead of the head)
+#ifndef CFGSIM_BIG_PF
+#define CFGSIM_BIG_PF 3
+#endif
+        constexpr int PF = CFGSIM_BIG_PF;  // prefetch depth (positions ahead of the head)
         unsigned long long hv[BIG_R], qv[BIG_R][PF];
         int hc[BIG_R], qc[BIG_R][PF], ptr[BIG_R];
         uint32_t act = 0u;
@@ -881,6 +914,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         }
         __syncthreads();
         if (prm.phase && tid == 0) atomicAdd(prm.phase + 7, (unsigned long long)N);
+        unsigned adv_steps = 0, adv_deep = 0;
         int prev_col = 0;
         for (int round = 0; round < N; round++) {
           unsigned long long bv = 0ull;
@@ -900,24 +934,22 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           const int wrow = (int)__reduce_min_sync(0xffffffffu, cand ? (unsigned)brow : 0x7fffffffu);
           const int buf = round & 1;
           if (wrow != 0x7fffffff && brow == wrow) {  // the owner lane publishes value, row, column
-            slot_v[buf * BIG_WARPS + warp] = bv;
-            slot_r[buf * BIG_WARPS + warp] = wrow;
-            slot_c[buf * BIG_WARPS + warp] = bcl;
+            gsl[buf * BIG_WARPS + warp] = make_ulonglong2(bv, ((unsigned long long)wrow << 32) | (unsigned)bcl);
           } else if (wrow == 0x7fffffff && lane == 0) {
-            slot_r[buf * BIG_WARPS + warp] = 0x7fffffff;
+            gsl[buf * BIG_WARPS + warp] = make_ulonglong2(0ull, 0x7fffffffull << 32);
           }
           __syncthreads();
           unsigned long long gv = 0ull;
           int grow = 0x7fffffff, bcol = 0;
 #pragma unroll
           for (int w = 0; w < BIG_WARPS; w++) {
-            const int rw = slot_r[buf * BIG_WARPS + w];
+            const ulonglong2 sl = gsl[buf * BIG_WARPS + w];
+            const int rw = (int)(sl.y >> 32);
             if (rw == 0x7fffffff) continue;
-            const unsigned long long v = slot_v[buf * BIG_WARPS + w];
-            if (grow == 0x7fffffff || v > gv || (v == gv && rw < grow)) {
-              gv = v;
+            if (grow == 0x7fffffff || sl.x > gv || (sl.x == gv && rw < grow)) {
+              gv = sl.x;
               grow = rw;
-              bcol = slot_c[buf * BIG_WARPS + w];
+              bcol = (int)(unsigned)sl.y;
             }
           }
           // taken columns, two generations: round r reads T_r from buffer r & 1
@@ -941,10 +973,9 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
             if (((act >> r) & 1u) && hc[r] == bcol) {
               const int i = tid + BIG_THREADS * r;
               int p = ptr[r];
-              int steps = 0;
+              const int p0 = p;
               do {  // p + 1 < N: an active row always has an untaken column
                 ++p;
-                ++steps;
                 hv[r] = qv[r][0];
                 hc[r] = qc[r][0];
 #pragma unroll
@@ -955,12 +986,14 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
                 }
               } while (hc[r] == bcol || ((tk_cur[hc[r] >> 5] >> (hc[r] & 31)) & 1u));
               ptr[r] = p;
-              if (prm.phase) {  // diagnostics: advances, advances past the prefetched window
-                atomicAdd(prm.phase + 5, (unsigned long long)steps);
-                if (steps > PF) atomicAdd(prm.phase + 6, 1ull);
-              }
+              adv_steps += (unsigned)(p - p0);  // diagnostics (registers; one atomic per pair)
+              adv_deep += (p - p0 > PF) ? 1u : 0u;
             }
           }
+        }
+        if (prm.phase) {  // advances, advances past the prefetched window
+          atomicAdd(prm.phase + 5, (unsigned long long)adv_steps);
+          atomicAdd(prm.phase + 6, (unsigned long long)adv_deep);
         }
         __syncthreads();
         if (tid == 0) {  // similarity.py:150: Python sum in row order

@@ -742,20 +742,24 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
       mrow[2 * brow + 1] = (int)(unsigned)wk;
     }
     taken |= 1ull << bcol;
+    // advance the rows whose head column was taken: the lane's rows'
+    // loads are issued side by side (one order load, one key load on the
+    // critical path when the next column is free, the common case)
+    bool adv[KB];
+    int col[KB];
 #pragma unroll
     for (int cc = 0; cc < KB; cc++) {
       if (lane + 32 * cc == brow) act[cc] = false;
-      if (act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol) {
-        const int i = lane + 32 * cc;
-        int p = ptr[cc], col;
-        do {
-          ++p;
-          col = ord[i * N + p];
-        } while ((taken >> col) & 1ull);
-        ptr[cc] = p;
-        hk[cc] = Kr[i * PK + col];
-      }
+      adv[cc] = act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol;
+      col[cc] = adv[cc] ? (int)ord[(lane + 32 * cc) * N + (++ptr[cc])] : 0;
     }
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++)
+      if (adv[cc])
+        while ((taken >> col[cc]) & 1ull) col[cc] = ord[(lane + 32 * cc) * N + (++ptr[cc])];
+#pragma unroll
+    for (int cc = 0; cc < KB; cc++)
+      if (adv[cc]) hk[cc] = Kr[(lane + 32 * cc) * PK + col[cc]];
   }
   __syncwarp();
   if (lane == 0)  // similarity.py:150: Python's sum, row order

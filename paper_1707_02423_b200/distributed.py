@@ -26,14 +26,41 @@ def row_starts(k: int) -> np.ndarray:
     return np.concatenate([[0], np.cumsum(np.arange(k, 0, -1))]).astype(np.int64)
 
 
+def _cost_table():
+    """(N samples, us per unit) of csrc/cost_model.h — the one table the C
+    split and this mirror share."""
+    import re
+    from pathlib import Path
+    txt = (Path(__file__).resolve().parent / "csrc" / "cost_model.h").read_text()
+    body = txt[txt.index("COST_TABLE_BEGIN"):txt.index("COST_TABLE_END")]
+    ns = [int(x) for x in re.search(r"kCostN\[\] = \{([^}]*)\}", body).group(1).split(",")]
+    us = [float(x) for x in re.search(r"kCostUs\[\] = \{([^}]*)\}", body).group(1).split(",")]
+    return np.array(ns, np.float64), np.array(us, np.float64)
+
+
+def unit_cost_us(n) -> np.ndarray:
+    """Measured per-unit cost vs N (cost_model.h: piecewise linear, clamped),
+    with the C routine's operation order (bitwise the same costs, hence the
+    same split)."""
+    xs, ys = _cost_table()
+    n = np.asarray(n, np.float64)
+    i = np.clip(np.searchsorted(xs, n, side="left"), 1, len(xs) - 1)
+    t = (n - xs[i - 1]) / (xs[i] - xs[i - 1])
+    out = ys[i - 1] + t * (ys[i] - ys[i - 1])
+    out = np.where(n <= xs[0], ys[0], out)
+    return np.where(n > xs[-1], ys[-1], out)
+
+
 def split_units(n_nodes: np.ndarray, world: int) -> np.ndarray:
-    """world+1 unit boundaries balancing sum N^2 per rank (N = n of the row's
-    graph; rows sorted by n descending, stable)."""
+    """world+1 unit boundaries balancing the measured cost per rank
+    (unit_cost_us of the row's N; rows sorted by n descending, stable) —
+    mirrors cfgsim_allpairs_split."""
     n_nodes = np.asarray(n_nodes)
     k = len(n_nodes)
     ns = n_nodes[np.argsort(-n_nodes, kind="stable")].astype(np.float64)
     rs = row_starts(k)
-    per_row = (k - np.arange(k)) * ns * ns
+    cost = unit_cost_us(ns)
+    per_row = (k - np.arange(k)) * cost
     cum = np.concatenate([[0.0], np.cumsum(per_row)])
     total = cum[-1]
     bounds = np.zeros(world + 1, np.int64)
@@ -41,7 +68,7 @@ def split_units(n_nodes: np.ndarray, world: int) -> np.ndarray:
         target = total * r / world
         a = int(np.searchsorted(cum, target, side="right")) - 1
         a_c = min(a, k - 1)
-        per = ns[a_c] * ns[a_c]
+        per = cost[a_c]
         u = rs[a] + int(np.ceil((target - cum[a]) / per))
         u = min(u, rs[min(a + 1, k)])
         bounds[r] = max(u, bounds[r - 1])

@@ -29,10 +29,11 @@ def test_split_covers_triangle_and_balances():
         b = split_units(n, world)
         assert b[0] == 0 and b[-1] == row_starts(len(n))[-1]
         assert (np.diff(b) >= 0).all()
-    # cost balance within a few percent at 8 ranks
+    # balance of the measured cost model (csrc/cost_model.h) within 2% at 8 ranks
+    from paper_1707_02423_b200.distributed import unit_cost_us
     from paper_1707_02423_b200.workload import triangle_units
     perm, a, _ = triangle_units(n)
-    cost = (n[perm[a]].astype(float)) ** 2
+    cost = unit_cost_us(n[perm[a]])
     b = split_units(n, 8)
     per = np.array([cost[b[r]:b[r + 1]].sum() for r in range(8)])
     assert per.max() / per.mean() < 1.02

@@ -46,55 +46,32 @@ def main() -> None:
     res = {}
     with P.DeviceCorpus(mats) as C:
         st = torch.cuda.current_stream().cuda_stream
-        # large / mid N: random pairs (row graph of size N, partner uniformly among n <= N)
-        for N in list(range(72, 513, 24)) + [65, 96, 128, 129, 160, 256, 257, 384, 512]:
-            rows = np.flatnonzero(n == N)
-            parts = np.flatnonzero(n <= N)
-            if len(rows) == 0:
-                continue
-            npairs = a.pairs if N > 128 else 4 * a.pairs
-            ia = rng.choice(rows, npairs).astype(np.int32)
-            ib = rng.choice(parts, npairs).astype(np.int32)
-            best = None
-            for rep in range(2):
-                torch.cuda.synchronize()
-                ev0.record()
-                P.isorank_pairs(C, C, ia, ib)
-                ev1.record()
-                torch.cuda.synchronize()
-                t = ev0.elapsed_time(ev1) * 1e3 / npairs
-                best = t if best is None else min(best, t)
-            res[N] = {"us_per_unit": best, "how": "isorank_pairs sample", "pairs": npairs}
-            print(N, res[N], flush=True)
-        # small N: two-stage ranges over the row group
+        # every sampled N: allpairs_range over whole rows of that N's row group
+        # (a row's partners are all smaller graphs: the mix the triangle has)
         order = np.argsort(-n, kind="stable")
         ns = n[order]
         k = len(n)
         rs = np.concatenate([[0], np.cumsum(np.arange(k, 0, -1))])
-        out = torch.empty(400000, dtype=torch.float64, device="cuda")
-        for N in (16, 24, 32, 40, 48, 56, 64):
+        out = torch.empty(500000, dtype=torch.float64, device="cuda")  # >= units of one measurement
+        for N in sorted(set(list(range(16, 513, 16)) + [65, 72, 96, 120, 129, 136, 144, 160, 176, 192, 257, 384])):
             grp = np.flatnonzero(ns == N)
             if len(grp) == 0:
                 continue
-            u0 = int(rs[grp[0]])
-            uend = int(rs[grp[-1] + 1])
+            budget = 60000 if N > 64 else 400000  # units per measurement
+            r1 = grp[0]
+            while r1 + 1 <= grp[-1] and rs[r1 + 1] - rs[grp[0]] < budget:
+                r1 += 1
+            u0, u1 = int(rs[grp[0]]), int(rs[r1 + 1])
             ts = []
-            for U in (100000, 200000):
-                U = min(U, uend - u0)
-                best = None
-                for rep in range(2):
-                    torch.cuda.synchronize()
-                    ev0.record()
-                    nat.check(nat.lib.cfgsim_allpairs_range(C.handle, u0, u0 + U, 0, nat.C.byref(prm), nat.ptr(out),
-                                                            None, st))
-                    ev1.record()
-                    torch.cuda.synchronize()
-                    t = ev0.elapsed_time(ev1) * 1e3
-                    best = t if best is None else min(best, t)
-                ts.append((U, best))
-            (U1, t1), (U2, t2) = ts
-            per = (t2 - t1) / (U2 - U1) if U2 > U1 else t2 / U2
-            res[N] = {"us_per_unit": per, "fixed_us": t1 - per * U1, "how": "allpairs_range slices", "units": [U1, U2]}
+            for rep in range(3):
+                torch.cuda.synchronize()
+                ev0.record()
+                nat.check(nat.lib.cfgsim_allpairs_range(C.handle, u0, u1, 0, nat.C.byref(prm), nat.ptr(out), None, st))
+                ev1.record()
+                torch.cuda.synchronize()
+                ts.append(ev0.elapsed_time(ev1) * 1e3 / (u1 - u0))
+            res[N] = {"us_per_unit": min(ts), "reps": [round(t, 4) for t in ts], "units": u1 - u0,
+                      "rows": int(r1 - grp[0] + 1)}
             print(N, res[N], flush=True)
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     Path(a.out).write_text(json.dumps({"graphs": a.graphs, "costs": {str(k): v for k, v in sorted(res.items())}},
