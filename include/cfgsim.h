@@ -193,6 +193,12 @@ CFGSIM_API int cfgsim_flat_allpairs(const cfgsim_corpus *c, int32_t measure, dou
  * EUC and JAC share sum (x-y)^2).  [host|device] output. */
 CFGSIM_API int cfgsim_flat_all_allpairs(const cfgsim_corpus *c, double p, double *d_mats, void *cuda_stream);
 
+/* Page-locked host memory for result arrays (the Python API returns K x K
+ * score matrices in reused pinned buffers: the device results land there by
+ * DMA, with no page faults on the host scatter). */
+CFGSIM_API int cfgsim_host_alloc(int64_t bytes, void **ptr);
+CFGSIM_API int cfgsim_host_free(void *ptr);
+
 /* Diagnostics (not on any alignment path): fp64 mma.sync.m8n8k4 and DFMA
  * throughput of the device in TFLOP/s, measured now (bench.py's roofline
  * denominator, at the clocks of the run). */

@@ -69,6 +69,8 @@ _SIGS = {
     "cfgsim_flat_allpairs": ([_vp, _i32, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_flat_all_allpairs": ([_vp, C.c_double, _vp, _vp], C.c_int),
     "cfgsim_probe_fp64": ([_i32, _vp, _vp], C.c_int),
+    "cfgsim_host_alloc": ([C.c_int64, C.POINTER(C.c_void_p)], C.c_int),
+    "cfgsim_host_free": ([_vp], C.c_int),
     "cfgsim_heatmap_csv": ([_i32, _vp, _vp, _vp, _vp, _i64, _vp, _i32], C.c_int),
     "cfgsim_ward": ([_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "cfgsim_matrices_from_listings": ([_i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.POINTER(_vp)], C.c_int),
@@ -135,3 +137,49 @@ def default_device() -> int:
 
 def launch_count() -> int:
     return int(lib.cfgsim_launch_count())
+
+
+class _PinnedBuffer:
+    """Page-locked host memory (cfgsim_host_alloc) exposed to numpy; freed
+    when the last array viewing it is gone."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        check(lib.cfgsim_host_alloc(int(nbytes), C.byref(p)))
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+        self.__array_interface__ = {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                                    "version": 3}
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.cfgsim_host_free(self.ptr)
+            self.ptr = None
+
+
+_PINNED: list = []  # [buffer, weakref of the array last handed out]
+
+
+def pinned_array(shape, dtype=np.float64) -> np.ndarray:
+    """An uninitialised array in page-locked memory for K x K results: a
+    buffer is reused once no array handed out from it is alive, so repeated
+    calls neither pin new memory nor fault fresh pages (device results land
+    by DMA; the host scatter writes resident pages)."""
+    import weakref
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    if nbytes < (1 << 20):
+        return np.empty(shape, dtype)
+    for ent in _PINNED:
+        buf, ref = ent
+        if buf.nbytes >= nbytes and (ref is None or ref() is None):
+            a = np.asarray(buf)[:nbytes].view(dtype).reshape(shape)
+            ent[1] = weakref.ref(a)
+            return a
+    try:
+        buf = _PinnedBuffer(nbytes)
+    except DeviceError:  # (no driver: plain host memory; the compute call itself will report it)
+        return np.empty(shape, dtype)
+    a = np.asarray(buf)[:nbytes].view(dtype).reshape(shape)
+    _PINNED.append([buf, weakref.ref(a)])
+    return a

@@ -70,6 +70,17 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// page-locked host memory (cudaHostAlloc / registered): D2H lands there directly
+bool is_pinned_host_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // RAII device buffer
 struct DBuf {
   void *p = nullptr;
@@ -260,7 +271,6 @@ struct Scratch {
   int64_t ovf_cap = 0;
   DBuf pool_lin, pool_it, pool_out[4];  // per-call outputs, grow-only (no cudaMalloc/cudaFree per call)
   PinBuf pin_out[4], pin_in;            // pinned staging of host outputs / corpus uploads
-  cudaStream_t copy_stream = nullptr;   // D2H of pipelined all-pairs chunks
   std::recursive_mutex mu;
   cudaEvent_t done = nullptr;  // recorded at the end of the last call's stream work
   int depth = 0;               // nesting of guards on the owning thread
@@ -953,10 +963,10 @@ struct OutStage {
       e = own.alloc(b);
       dev = own.p;
     }
-    if (e == cudaSuccess && pinb && b >= (1u << 20)) {
+    if (e == cudaSuccess && pinb && b >= (1u << 20) && !is_pinned_host_ptr(u)) {
       e = pinb->grow(b);  // (the previous user of this buffer synchronised before returning)
       if (e == cudaSuccess) pin = pinb;
-    }
+    }  // (a page-locked caller buffer receives the D2H directly: no staging copy)
     return e;
   }
   cudaError_t finish(cudaStream_t st) {
@@ -1708,89 +1718,6 @@ int cfgsim_allpairs_scatter(const cfgsim_corpus *c, int32_t ordered, const doubl
   return CFGSIM_OK;
 }
 
-// Host-output all-pairs as a pipeline: the unit triangle in cost-balanced
-// chunks; chunk j's unit-linear results go to pinned host memory on a copy
-// stream as soon as its kernels finish, and host threads scatter them into
-// the caller's K x K matrices (both triangles, caller's graph order) while
-// the GPU computes chunk j + 1.  Only the last chunk's copy and scatter are
-// exposed after the kernels (the one-shot path: device scatter, 32 MB D2H of
-// the full matrix and a host copy, all after the last kernel).
-int allpairs_host_pipelined(const cfgsim_corpus *c, const cfgsim_params *p, double *d_mat, int32_t *iters_mat,
-                            cudaStream_t st) {
-  const int64_t nu = c->row_start[c->K];
-  const int K = c->K;
-  Scratch &S = scratch_for(c->device);
-  CU(grow_buf(S.pool_lin, sizeof(double) * nu, st));
-  if (iters_mat) CU(grow_buf(S.pool_it, sizeof(int32_t) * nu, st));
-  CU(S.pin_out[0].grow(sizeof(double) * nu));
-  if (iters_mat) CU(S.pin_out[1].grow(sizeof(int32_t) * nu));
-  double *dl = S.pool_lin.as<double>();
-  int32_t *il = iters_mat ? S.pool_it.as<int32_t>() : nullptr;
-  double *hd = (double *)S.pin_out[0].p;
-  int32_t *hi = iters_mat ? (int32_t *)S.pin_out[1].p : nullptr;
-  const int nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(6, nu / 20000));
-  std::vector<int64_t> b(nchunk + 1);
-  if (int rc = cfgsim_allpairs_split(c, nchunk, b.data())) return rc;
-  if (!S.copy_stream) CU(cudaStreamCreateWithFlags(&S.copy_stream, cudaStreamNonBlocking));
-  std::vector<cudaEvent_t> done(nchunk, nullptr), copied(nchunk, nullptr);
-  auto cleanup = [&] {
-    for (auto e : done) if (e) cudaEventDestroy(e);
-    for (auto e : copied) if (e) cudaEventDestroy(e);
-  };
-  for (int j = 0; j < nchunk; j++) {
-    CU(cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&copied[j], cudaEventDisableTiming));
-  }
-  for (int j = 0; j < nchunk; j++) {
-    const int64_t u0 = b[j], u1 = b[j + 1];
-    if (u1 > u0) {
-      if (int rc = cfgsim_allpairs_range(c, u0, u1, 0, p, dl + u0, il ? il + u0 : nullptr, st)) {
-        cleanup();
-        return rc;
-      }
-    }
-    CU(cudaEventRecord(done[j], st));
-    CU(cudaStreamWaitEvent(S.copy_stream, done[j], 0));
-    if (u1 > u0) {
-      CU(cudaMemcpyAsync(hd + u0, dl + u0, sizeof(double) * (u1 - u0), cudaMemcpyDeviceToHost, S.copy_stream));
-      if (hi) CU(cudaMemcpyAsync(hi + u0, il + u0, sizeof(int32_t) * (u1 - u0), cudaMemcpyDeviceToHost, S.copy_stream));
-    }
-    CU(cudaEventRecord(copied[j], S.copy_stream));
-  }
-  // host scatter of each chunk as it lands (unit u -> sorted rows a <= b;
-  // the matrix entries (perm[a], perm[b]) and (perm[b], perm[a]))
-  const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const auto &rs = c->row_start;
-  const auto &perm = c->perm;
-  for (int j = 0; j < nchunk; j++) {
-    CU(cudaEventSynchronize(copied[j]));
-    const int64_t u0 = b[j], u1 = b[j + 1];
-    const int64_t per = (u1 - u0 + nt - 1) / nt;
-    auto work = [&](int t) {
-      const int64_t s0 = u0 + per * t, s1 = std::min(u1, s0 + per);
-      if (s0 >= s1) return;
-      int64_t a = (int64_t)(std::upper_bound(rs.begin(), rs.end(), s0) - rs.begin()) - 1;
-      for (int64_t u = s0; u < s1; u++) {
-        while (rs[a + 1] <= u) a++;
-        const int64_t bb = a + (u - rs[a]);
-        const size_t x = (size_t)perm[a], y = (size_t)perm[bb];
-        d_mat[x * K + y] = hd[u];
-        d_mat[y * K + x] = hd[u];
-        if (iters_mat) {
-          iters_mat[x * K + y] = hi[u];
-          iters_mat[y * K + x] = hi[u];
-        }
-      }
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; t++) pool.emplace_back(work, t);
-    work(0);
-    for (auto &th : pool) th.join();
-  }
-  cleanup();
-  return CFGSIM_OK;
-}
-
 int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params *p,
                     double *d_mat, int32_t *iters_mat, void *cuda_stream) {
   CFGSIM_NVTX("cfgsim.allpairs");
@@ -1799,15 +1726,6 @@ int cfgsim_allpairs(const cfgsim_corpus *c, int32_t ordered, const cfgsim_params
   if (int rc = set_device(c->device)) return rc;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   DeviceGuard guard(c->device, st);
-  static const bool pipelined = [] {  // CFGSIM_PIPELINE=0: the one-shot path (A/B)
-    const char *e = getenv("CFGSIM_PIPELINE");
-    return !(e && std::string(e) == "0");
-  }();
-  if (pipelined && !ordered && !is_device_ptr(d_mat) && (!iters_mat || !is_device_ptr(iters_mat))) {
-    int rc = allpairs_host_pipelined(c, p, d_mat, iters_mat, st);
-    if (rc == CFGSIM_OK) CU(cudaStreamSynchronize(st));
-    return rc;
-  }
   const int64_t nu = c->row_start[c->K];
   const int64_t slots = ordered ? 2 * nu : nu;
   Scratch &S = scratch_for(c->device);
@@ -2257,6 +2175,19 @@ __global__ void probe_dfma_kernel(double *out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 }  // namespace
+
+int cfgsim_host_alloc(int64_t bytes, void **ptr) {
+  if (!ptr || bytes < 0) return fail(CFGSIM_ERR_ARG, "bad arguments");
+  *ptr = nullptr;
+  if (bytes == 0) return CFGSIM_OK;
+  CU(cudaHostAlloc(ptr, (size_t)bytes, cudaHostAllocPortable));
+  return CFGSIM_OK;
+}
+
+int cfgsim_host_free(void *ptr) {
+  if (ptr) CU(cudaFreeHost(ptr));
+  return CFGSIM_OK;
+}
 
 int cfgsim_probe_fp64(int32_t device, double *mma_tflops, double *fma_tflops) {
   if (int rc = set_device(device)) return rc;

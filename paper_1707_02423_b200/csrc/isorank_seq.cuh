@@ -712,7 +712,10 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
   unsigned long long hk[KB];
   int ptr[KB];
   bool act[KB];
-  unsigned long long taken = 0ull;
+  uint32_t tk[KB];  // taken columns, 32 per word (32-bit tests on the advance path)
+#pragma unroll
+  for (int q = 0; q < KB; q++) tk[q] = 0u;
+  auto taken_col = [&](int c) { return ((KB > 1 && c >= 32 ? tk[KB - 1] : tk[0]) >> (c & 31)) & 1u; };
 #pragma unroll
   for (int cc = 0; cc < KB; cc++) {
     const int i = lane + 32 * cc;
@@ -741,7 +744,7 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
       mrow[2 * brow] = (int)(unsigned)(wk >> 32);  // winning key (value bits) for W
       mrow[2 * brow + 1] = (int)(unsigned)wk;
     }
-    taken |= 1ull << bcol;
+    if (KB > 1 && bcol >= 32) tk[KB - 1] |= 1u << (bcol & 31); else tk[0] |= 1u << (bcol & 31);
     // advance the rows whose head column was taken: the lane's rows'
     // loads are issued side by side (one order load, one key load on the
     // critical path when the next column is free, the common case)
@@ -756,7 +759,7 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
 #pragma unroll
     for (int cc = 0; cc < KB; cc++)
       if (adv[cc])
-        while ((taken >> col[cc]) & 1ull) col[cc] = ord[(lane + 32 * cc) * N + (++ptr[cc])];
+        while (taken_col(col[cc])) col[cc] = ord[(lane + 32 * cc) * N + (++ptr[cc])];
 #pragma unroll
     for (int cc = 0; cc < KB; cc++)
       if (adv[cc]) hk[cc] = Kr[(lane + 32 * cc) * PK + col[cc]];

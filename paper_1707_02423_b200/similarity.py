@@ -211,7 +211,7 @@ def pairwise(matrices: list[TransitionMatrix], measure: MeasureId, *, p: float =
         pm = PairwiseMatrix(measure=measure, kernel_ids=ids, scores=scores, scaled=False)
         return (pm, None) if return_iterations else pm
     _check_alpha(alpha)
-    scores = np.empty((k, k))
+    scores = nat.pinned_array((k, k))
     iters = np.empty((k, k), np.int32) if return_iterations else None
     prm = nat.params(alpha, tol, max_iter, precision)
     with DeviceCorpus(ordered, _dev(device)) as corpus:
