@@ -1681,12 +1681,24 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
     unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no % 64);
     if (big) {
       if (int rc = big_launch(p->precision, N, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
-    } else if (lr) {
-      if (int rc = lr_launch(p->precision, N, false, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
     } else {
-      if (int rc = launch_tier(p->precision, pl.ti, N, cap_for(p->precision, pl, N, false), c->dev(), c->dev(),
-                               w, o, p, ctr, st))
+      // per-pair kernels with operator lists: records of overflowed /
+      // ambiguous pairs, handled after every launch so that the list never
+      // needs more than one launch's units (a full C5 rank range has
+      // millions of mid-N pairs)
+      if (S.ovf_cap < w.n_items) {
+        CU(cudaStreamSynchronize(st));
+        if (int rc = ensure_scratch(S, w.n_items)) return rc;
+        o.ovf_list = S.ovf_list.as<int64_t>();
+        o.ovf_cap = (int32_t)std::min<int64_t>(S.ovf_cap, INT32_MAX);
+      }
+      if (lr) {
+        if (int rc = lr_launch(p->precision, N, false, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
+      } else if (int rc = launch_tier(p->precision, pl.ti, N, cap_for(p->precision, pl, N, false), c->dev(),
+                                      c->dev(), w, o, p, ctr, st)) {
         return rc;
+      }
+      if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
     }
     launch_no++;
     u = seg_end;

@@ -257,6 +257,29 @@ __device__ __forceinline__ T big_t_entry(const BigSide &S, const T *u, int c) {
   return (T)acc;
 }
 
+// phase 1a (interpolated sides): s_r = sum_{lo_p = r} (1-fr_p) y_p +
+// sum_{lo_p = r-1} fr_p y_p, y = D^-1 u — the same fma chain big_t_entry
+// forms inline, computed once per source row r instead of once per entry
+// of column r in every column's sum (deg_in(r) times, by only n threads)
+template <typename T>
+__device__ __forceinline__ double big_s_entry(const BigSide &S, const T *u, int r) {
+  const int n = S.n;
+  double s = 0.0;
+  if (r <= n - 2)
+    for (int p = S.pst[r]; p < S.pst[r + 1]; p++) s = fma(1.0 - S.fr[p], (double)u[p] * S.rinv[p], s);
+  if (r >= 1)
+    for (int p = S.pst[r - 1]; p < S.pst[r]; p++) s = fma(S.fr[p], (double)u[p] * S.rinv[p], s);
+  return s;
+}
+
+// phase 1b: t[c] = sum_r A[r, c] s_r over column c (bitwise big_t_entry)
+template <typename T>
+__device__ __forceinline__ T big_t_from_s(const BigSide &S, const double *sb, int c) {
+  double acc = 0.0;
+  for (int e = S.cp[c]; e < S.cp[c + 1]; e++) acc = fma(S.cv[e], sb[S.cr[e]], acc);
+  return (T)acc;
+}
+
 // phase 2: u'[q] = (W t)[q] + zsum / N
 template <typename T>
 __device__ __forceinline__ T big_u_entry(const BigSide &S, const T *t, int q, double zterm) {
@@ -447,6 +470,8 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       setup(SA, C1, g1, 0);
       setup(SB, C2, g2, 1);
       T *ring[2] = {(T *)(smem_raw + L.ring[0]), (T *)(smem_raw + L.ring[1])};
+      double *sbuf = (double *)(smem_raw + L.scr);  // s per source row (2 sides, nlim each); free after setup
+      const int nlim_s = prm.nlim;
       T *tv[2] = {(T *)(smem_raw + L.t[0]), (T *)(smem_raw + L.t[1])};
 
       BIG_PHASE(1);
@@ -466,15 +491,26 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       __syncthreads();
       for (;; k++) {
         const int cur = (k - 1) & 1, nxt = k & 1;  // ring slots of u_{k-1}, u_k
-        // phase 1: t = A^T W^T D^-1 u_{k-1}
+        // phase 1: t = A^T W^T D^-1 u_{k-1}; interpolated sides in two steps
+        // (s = W^T D^-1 u per source row into the operator-build scratch,
+        // then the column sums), identical arithmetic to the fused form
         {
           const int n0 = SA.kind == 2 ? 0 : SA.n;
           const int n1 = SB.kind == 2 ? 0 : SB.n;
+          if (SA.kind == 1 || SB.kind == 1) {
+            const int m0 = SA.kind == 1 ? SA.n : 0, m1 = SB.kind == 1 ? SB.n : 0;
+            for (int q = tid; q < m0 + m1; q += NT) {
+              if (q < m0) sbuf[q] = big_s_entry<T>(SA, ring[0] + cur * N, q);
+              else sbuf[nlim_s + q - m0] = big_s_entry<T>(SB, ring[1] + cur * N, q - m0);
+            }
+            __syncthreads();
+          }
           for (int q = tid; q < n0 + n1; q += NT) {
             if (q < n0)
-              tv[0][q] = big_t_entry<T>(SA, ring[0] + cur * N, q);
+              tv[0][q] = SA.kind == 1 ? big_t_from_s<T>(SA, sbuf, q) : big_t_entry<T>(SA, ring[0] + cur * N, q);
             else
-              tv[1][q - n0] = big_t_entry<T>(SB, ring[1] + cur * N, q - n0);
+              tv[1][q - n0] = SB.kind == 1 ? big_t_from_s<T>(SB, sbuf + nlim_s, q - n0)
+                                           : big_t_entry<T>(SB, ring[1] + cur * N, q - n0);
           }
         }
         __syncthreads();
@@ -869,7 +905,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
 
       BIG_PHASE(4);
       // ---- 4b. greedy matching rounds, similarity.py:96-108, whole CTA.
-      // Thread t owns rows t + 256 r (r < BIG_R); each active row's head is
+      // Thread t owns rows t + 256 r (r < R); each active row's head is
       // its best untaken column, compared across rows on exact value bits
       // with ties to the lowest row (np.argmax's first occurrence).  A round:
       // per-warp best -> shared slots (value, row, column) -> one barrier ->
@@ -885,15 +921,22 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         int32_t *mrow = (int32_t *)(smem_raw + L.mrow);
         unsigned long long *mval = (unsigned long long *)(smem_raw + L.mval);
         for (int w = tid; w < 64; w += NT) taken[w] = 0u;
+        // rows per thread R = N-bound / 256 (1, 2, 4 for KB = 8, 16, 32) and
+        // a register window of PF = 12 / R sorted entries per row (the same
+        // 36 registers in every variant): the shorter rows of the smaller
+        // classes get a deeper window, so fewer head advances ("deep skips"
+        // past taken columns) wait on a dependent HBM load inside a round
+        constexpr int R = (32 * KB) / BIG_THREADS < 1 ? 1 : (32 * KB) / BIG_THREADS;
 #ifndef CFGSIM_BIG_PF
-#define CFGSIM_BIG_PF 3
+        constexpr int PF = 12 / R;
+#else
+        constexpr int PF = CFGSIM_BIG_PF;
 #endif
-        constexpr int PF = CFGSIM_BIG_PF;  // prefetch depth (positions ahead of the head)
-        unsigned long long hv[BIG_R], qv[BIG_R][PF];
-        int hc[BIG_R], qc[BIG_R][PF], ptr[BIG_R];
+        unsigned long long hv[R], qv[R][PF];
+        int hc[R], qc[R][PF], ptr[R];
         uint32_t act = 0u;
 #pragma unroll
-        for (int r = 0; r < BIG_R; r++) {
+        for (int r = 0; r < R; r++) {
           const int i = tid + BIG_THREADS * r;
           hv[r] = 0ull;
           hc[r] = 0;
@@ -920,7 +963,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           unsigned long long bv = 0ull;
           int brow = 0x7fffffff, bcl = 0;
 #pragma unroll
-          for (int r = 0; r < BIG_R; r++)
+          for (int r = 0; r < R; r++)
             if (((act >> r) & 1u) && (brow == 0x7fffffff || hv[r] > bv)) {
               bv = hv[r];
               brow = tid + BIG_THREADS * r;
@@ -969,7 +1012,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           }
           // advance rows whose head column was taken
 #pragma unroll
-          for (int r = 0; r < BIG_R; r++) {
+          for (int r = 0; r < R; r++) {
             if (((act >> r) & 1u) && hc[r] == bcol) {
               const int i = tid + BIG_THREADS * r;
               int p = ptr[r];

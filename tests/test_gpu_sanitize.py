@@ -1,9 +1,8 @@
-"""compute-sanitizer memcheck over small runs of the benchmark paths (``-m gpu``).
+"""compute-sanitizer memcheck / racecheck / synccheck over small runs of the benchmark paths (``-m gpu``).
 
-The full sweep (memcheck, racecheck, synccheck on reduced c2 / c3 / c4) is
-``tools/sanitize.sh``; its logs are summarised in ``profiles/``.  This test
-keeps the two paths that had a finding in round 1 under memcheck on every
-GPU test run.
+The full sweep (larger sizes) is ``tools/sanitize.sh``; its logs are
+summarised in ``profiles/r02_sanitize.txt``.  This gate runs all three tools
+on every GPU test run at sizes that finish in seconds to a minute.
 """
 
 from __future__ import annotations
@@ -22,12 +21,28 @@ REPO = Path(__file__).resolve().parents[1]
 CS = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
-@pytest.mark.parametrize("args", [["c3small", "--queries", "24", "--graphs", "1200"], ["c2", "--graphs", "40"]])
-def test_memcheck_clean(gpu, args):
+CASES = [
+    ("memcheck", ["c3small", "--queries", "24", "--graphs", "1200"]),
+    ("memcheck", ["c2", "--graphs", "40"]),
+    ("memcheck", ["c4", "--graphs", "4"]),
+    ("racecheck", ["c2", "--graphs", "24"]),        # the stage-2 named-barrier producer/consumer kernel
+    ("racecheck", ["c3small", "--queries", "8", "--graphs", "200"]),
+    ("synccheck", ["c2", "--graphs", "48"]),
+    ("synccheck", ["c4", "--graphs", "3"]),
+]
+
+
+@pytest.mark.parametrize("tool,args", CASES, ids=[f"{t}-{a[0]}" for t, a in CASES])
+def test_sanitizer_clean(gpu, tool, args):
+    """compute-sanitizer gate: memcheck / racecheck / synccheck
+    over reduced benchmark paths; each run is also a bitwise parity run of the
+    triangle / query path against the per-pair list path."""
     if not os.path.exists(CS):
         pytest.skip("compute-sanitizer not present")
-    r = subprocess.run([CS, "--tool", "memcheck", "--error-exitcode", "99", "--print-limit", "20", sys.executable,
+    r = subprocess.run([CS, "--tool", tool, "--error-exitcode", "99", "--print-limit", "20", sys.executable,
                         str(REPO / "tools" / "sanitize_run.py"), *args], capture_output=True, text=True, timeout=900,
                        cwd=REPO)
-    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
-    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert ("RACECHECK SUMMARY: 0 hazards" in out) if tool == "racecheck" else ("ERROR SUMMARY: 0 errors" in out)
+    assert "bitwise: True" in out

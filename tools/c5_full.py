@@ -29,6 +29,7 @@ def main() -> None:
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--parity", type=int, default=1500)
     ap.add_argument("--out", default="gpurun_out/c5_full.json")
+    ap.add_argument("--ranks", default=None, help="comma-separated subset of ranks to run (default: all)")
     a = ap.parse_args()
     import torch
 
@@ -55,7 +56,8 @@ def main() -> None:
                                                 nat.ptr(d_lin[nu - 20000:]), nat.ptr(it_lin[nu - 20000:]), st))
         torch.cuda.synchronize()
         ms = []
-        for r in range(a.world):
+        ranks = range(a.world) if a.ranks is None else [int(x) for x in a.ranks.split(",")]
+        for r in ranks:
             u0, u1 = int(b[r]), int(b[r + 1])
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -67,15 +69,18 @@ def main() -> None:
             print(f"rank {r}: units [{u0}, {u1}) {u1 - u0} alignments, {ms[-1]:.1f} ms "
                   f"({(u1 - u0) / ms[-1] * 1e3:.0f} pairs/s)", flush=True)
         tot = sum(ms)
-        res.update({"units": nu, "bounds": [int(x) for x in b], "rank_ms": ms, "total_ms_1gpu": tot,
-                    "pairs_per_s_1gpu": nu / tot * 1e3, "imbalance_max_over_mean": max(ms) / (tot / a.world),
-                    "projected_step_ms_at_world": max(ms),
-                    "projected_pairs_per_s_at_world": nu / max(ms) * 1e3})
+        res.update({"units": nu, "bounds": [int(x) for x in b], "ranks_run": list(ranks), "rank_ms": ms})
+        if len(ms) == a.world:
+            res.update({"total_ms_1gpu": tot, "pairs_per_s_1gpu": nu / tot * 1e3,
+                        "imbalance_max_over_mean": max(ms) / (tot / a.world), "projected_step_ms_at_world": max(ms),
+                        "projected_pairs_per_s_at_world": nu / max(ms) * 1e3})
         # parity of a random unit sample (the checker, after the timed ranges)
         if a.parity:
             from oracle import ffi
             rng = np.random.default_rng(0)
-            us = np.sort(rng.choice(nu, a.parity, replace=False))
+            lo_u = int(b[min(ranks)])
+            hi_u = int(b[max(ranks) + 1])
+            us = np.unique(rng.integers(lo_u, hi_u, 2 * a.parity))[: a.parity]
             perm, ai, bi = workload.triangle_units(C.n_nodes)
             ga, gb = perm[ai[us]], perm[bi[us]]
             lo, hi = np.minimum(ga, gb), np.maximum(ga, gb)
@@ -83,7 +88,7 @@ def main() -> None:
             d_ref, _, it_ref, _ = ffi.iso_batch(P.pack(mats), lo.astype(np.int32), hi.astype(np.int32))
             got_d = d_lin.cpu().numpy()[us]
             got_it = it_lin.cpu().numpy()[us]
-            res["parity"] = {"pairs": int(a.parity), "iter_mismatches": int((got_it != it_ref).sum()),
+            res["parity"] = {"pairs": int(len(us)), "iter_mismatches": int((got_it != it_ref).sum()),
                              "max_rel_err": float(np.max(np.abs(got_d - d_ref) / d_ref)),
                              "oracle_seconds": round(time.time() - t1, 1)}
             print("parity", res["parity"], flush=True)
