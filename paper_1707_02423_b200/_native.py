@@ -153,7 +153,10 @@ class _PinnedBuffer:
 
     def __del__(self):
         if getattr(self, "ptr", None):
-            lib.cfgsim_host_free(self.ptr)
+            try:
+                lib.cfgsim_host_free(self.ptr)
+            except Exception:  # (interpreter shutdown: the module is already torn down)
+                pass
             self.ptr = None
 
 

@@ -9,6 +9,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -79,6 +84,43 @@ bool is_pinned_host_ptr(const void *p) {
     return false;
   }
   return a.type == cudaMemoryTypeHost;
+}
+
+// cudaFuncSetAttribute + occupancy query, cached per (device, kernel, block,
+// smem): both are host round trips into the driver, and a C2 step launches
+// ~50 stage-2 / stage-1 kernels
+cudaError_t cached_occupancy(const void *fn, int threads, size_t smem, int *occ) {
+  struct Key {
+    int dev;
+    const void *fn;
+    int threads;
+    size_t smem;
+    bool operator<(const Key &o) const {
+      return std::tie(dev, fn, threads, smem) < std::tie(o.dev, o.fn, o.threads, o.smem);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  static std::map<std::pair<int, const void *>, size_t> attr;  // max dynamic smem already set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  const Key k{dev, fn, threads, smem};
+  auto it = cache.find(k);
+  if (it != cache.end()) {
+    *occ = it->second;
+    return cudaSuccess;
+  }
+  size_t &cur = attr[{dev, fn}];
+  if (smem > cur) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cur = smem;
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, threads, smem);
+  if (e == cudaSuccess) cache[k] = *occ;
+  return e;
 }
 
 // RAII device buffer
@@ -272,6 +314,9 @@ struct Scratch {
   DBuf pool_lin, pool_it, pool_out[4];  // per-call outputs, grow-only (no cudaMalloc/cudaFree per call)
   PinBuf pin_out[4], pin_in;            // pinned staging of host outputs / corpus uploads
   std::recursive_mutex mu;
+  // device buffers of destroyed corpora, reused by the next corpus of a
+  // similar size (no cudaMalloc / cudaFree — which synchronises — per call)
+  std::vector<std::pair<size_t, void *>> corpus_free;
   cudaEvent_t done = nullptr;  // recorded at the end of the last call's stream work
   int depth = 0;               // nesting of guards on the owning thread
 };
@@ -327,12 +372,11 @@ int launch_tier(int precision, int ti, int nlim, int cap, const DevCorpus &A, co
   const Tier &T = tiers(precision)[ti];
   const size_t smem = T.smem(nlim, cap);
   if (smem > kMaxSmem) return fail(CFGSIM_ERR_ARG, "tier shared memory exceeds 227 KB");
-  CU(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev;
   CU(cudaGetDevice(&dev));
   int sms = 0, occ = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, T.fn, T.nw * 32, smem));
+  CU(cached_occupancy((const void *)T.fn, T.nw * 32, smem, &occ));
   if (occ < 1) return fail(CFGSIM_ERR_CUDA, "tier kernel cannot be resident (occupancy 0)");
   int64_t grid = (int64_t)sms * occ;
   if (grid > work.n_items) grid = work.n_items;
@@ -439,11 +483,10 @@ int lr_launch(int precision, int nlim, bool dense_lists, const DevCorpus &A, con
   const size_t smem = L.total;
   prm.gslab = nullptr;
   prm.gslab_bytes = (int64_t)L.gtotal;
-  CU(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev, sms = 0, occ = 0;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, T.fn, nt, smem));
+  CU(cached_occupancy((const void *)T.fn, nt, smem, &occ));
   if (occ < 1) return fail(CFGSIM_ERR_CUDA, "low-rank kernel cannot be resident (occupancy 0)");
   int64_t grid = std::min<int64_t>((int64_t)sms * occ, work.n_items);
   if (grid < 1) return CFGSIM_OK;
@@ -511,11 +554,10 @@ int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, 
   const size_t slab = precision == CFGSIM_FP32 ? big_slab_layout<float>(nlim, prm.kcap).total
                                                : big_slab_layout<double>(nlim, prm.kcap).total;
   if (smem > kMaxSmem) return fail(CFGSIM_ERR_ARG, "large-N kernel shared memory exceeds 227 KB");
-  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev, sms = 0, occ = 0;
   CU(cudaGetDevice(&dev));
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BIG_THREADS, smem));
+  CU(cached_occupancy((const void *)fn, BIG_THREADS, smem, &occ));
   if (occ < 1) return fail(CFGSIM_ERR_CUDA, "large-N kernel cannot be resident (occupancy 0)");
   const int64_t grid = std::min<int64_t>((int64_t)sms * occ, work.n_items);
   if (grid < 1) return CFGSIM_OK;
@@ -561,8 +603,20 @@ int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, 
 }
 
 // internal-error flag of the large-N kernel (synchronises the stream)
+bool stream_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
 int big_status(Scratch &S, cudaStream_t st) {
   if (!S.status.p) return CFGSIM_OK;
+  // (a CUDA-graph capture cannot read it back; the flag is an internal
+  // assertion the bracket makes unreachable, checked on every eager call)
+  if (stream_capturing(st)) return CFGSIM_OK;
   int32_t v = 0;
   CU(cudaMemcpyAsync(&v, S.status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -685,9 +739,8 @@ int seq_stage1(const cfgsim_corpus *C, int64_t id0, int64_t n, const SeqRun &rr,
     const void *fk = pass == 0 ? (const void *)isorank_seq4_kernel<T, 2> : f1;
     const int nthr = pass == 0 ? 32 * SEQ4 : 128;
     const size_t smem = pass == 0 ? seq4_smem_layout<T>(kSeqNmax, sp.cap).total : seq_smem_layout<T>(kSeqNmax, sp.cap).total;
-    CU(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fk, nthr, smem));
+    CU(cached_occupancy((const void *)fk, nthr, smem, &occ));
     if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-1 kernel cannot be resident");
     const int64_t units = pass == 0 ? (cb.n + SEQ4 - 1) / SEQ4 : cb.n;
     const int64_t grid = std::min<int64_t>((int64_t)sms * occ, units);
@@ -731,9 +784,8 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
                          : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
                                           : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
   const size_t smem = p2_smem_bytes(N, sizeof(T), rr.kcap);
-  CU(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f2, nt, smem));
+  CU(cached_occupancy((const void *)f2, nt, smem, &occ));
   if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-2 kernel cannot be resident");
   const int64_t grid = std::min<int64_t>((int64_t)sms * occ, w.n_items);
   unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no++ % 64);
@@ -1283,27 +1335,82 @@ int check_flat(int32_t measure, double p) {
 
 // ====================================================================== C ABI
 namespace {
+// Persistent host worker pool for the graph-parallel packing passes (thread
+// creation per pass cost ~3-5 ms on a C2-sized corpus, several passes per
+// corpus).  One job at a time; the caller participates.
+class HostPool {
+ public:
+  static HostPool &get() {
+    static HostPool pool;
+    return pool;
+  }
+  int size() const { return (int)th_.size() + 1; }
+  void run(const std::function<void()> &work) {
+    std::lock_guard<std::mutex> serial(run_mu_);
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = &work;
+      active_ = (int)th_.size();
+      gen_++;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    job_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : th_) t.join();
+  }
+
+ private:
+  HostPool() {
+    const char *e = getenv("CFGSIM_HOST_THREADS");  // host packing threads (default: all cores, <= 32)
+    const int n = e && atoi(e) > 0 ? atoi(e) : std::min(32, (int)std::thread::hardware_concurrency());
+    for (int t = 1; t < n; t++) th_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    int seen = 0;
+    for (;;) {
+      const std::function<void()> *j;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        j = job_;
+      }
+      (*j)();
+      std::lock_guard<std::mutex> lk(m_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void()> *job_ = nullptr;
+  int gen_ = 0, active_ = 0;
+  bool stop_ = false;
+};
+
 // run f(g) for g in [0, n) on the host cores (graph-parallel packing)
 template <typename F>
 void parallel_graphs(int n, F f) {
-  static const int cap = [] {  // CFGSIM_HOST_THREADS: host packing threads (default: all cores, <= 32)
-    const char *e = getenv("CFGSIM_HOST_THREADS");
-    return e && atoi(e) > 0 ? atoi(e) : std::min(32, (int)std::thread::hardware_concurrency());
-  }();
-  const int nt = std::max(1, std::min<int>(cap, n / 64 + 1));
-  if (nt == 1) {
+  if (n < 64) {
     for (int g = 0; g < n; g++) f(g);
     return;
   }
   std::atomic<int> next{0};
-  auto work = [&]() {
+  const std::function<void()> work = [&]() {
     for (int g0; (g0 = next.fetch_add(32)) < n;)
       for (int g = g0; g < std::min(n, g0 + 32); g++) f(g);
   };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < nt; t++) pool.emplace_back(work);
-  work();
-  for (auto &t : pool) t.join();
+  HostPool::get().run(work);
 }
 
 // CSC of every graph (rows ascending within a column), same offsets as the
@@ -1404,9 +1511,25 @@ int corpus_create_impl(int32_t device, int32_t n_graphs, const int32_t *n_nodes,
     pt.at = total;
     total += (pt.bytes + 255) & ~size_t(255);
   }
-  cudaError_t e = c->d_all.alloc(std::max<size_t>(total, 256));
+  Scratch &S = scratch_for(device);
+  cudaError_t e = cudaSuccess;
+  {
+    std::lock_guard<std::recursive_mutex> lk(S.mu);
+    const size_t want = std::max<size_t>(total, 256);
+    int best = -1;
+    for (int q = 0; q < (int)S.corpus_free.size(); q++)
+      if (S.corpus_free[q].first >= want && S.corpus_free[q].first <= 2 * want + (1u << 20) &&
+          (best < 0 || S.corpus_free[q].first < S.corpus_free[best].first))
+        best = q;
+    if (best >= 0) {
+      c->d_all.p = S.corpus_free[best].second;
+      c->d_all.n = S.corpus_free[best].first;
+      S.corpus_free.erase(S.corpus_free.begin() + best);
+    } else {
+      e = c->d_all.alloc(want);
+    }
+  }
   if (e == cudaSuccess) {
-    Scratch &S = scratch_for(device);
     std::lock_guard<std::recursive_mutex> lk(S.mu);
     e = S.pin_in.grow(total);
     if (e == cudaSuccess) {
@@ -1523,6 +1646,10 @@ int cfgsim_corpus_destroy(cfgsim_corpus *c) {
     Scratch &S = scratch_for(c->device);
     std::lock_guard<std::recursive_mutex> lk(S.mu);
     S.seq_key.clear();  // a new corpus may reuse this address
+    if (c->d_all.p && S.corpus_free.size() < 4) {  // keep the buffer for the next corpus
+      S.corpus_free.push_back({c->d_all.n, c->d_all.p});
+      c->d_all.p = nullptr;
+    }
     delete c;
   }
   return CFGSIM_OK;
@@ -1616,6 +1743,7 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   if (int rc = check_params(p)) return rc;
   if (int rc = set_device(c->device)) return rc;
   if (u1 == u0) return CFGSIM_OK;
+  cudaGetLastError();  // (a stale non-sticky error of an unrelated earlier call is not this call's)
   if ((d_lin && !is_device_ptr(d_lin)) || (iters_lin && !is_device_ptr(iters_lin)))
     return fail(CFGSIM_ERR_ARG, "allpairs_range outputs must be device pointers");
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -1686,6 +1814,9 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
       // ambiguous pairs, handled after every launch so that the list never
       // needs more than one launch's units (a full C5 rank range has
       // millions of mid-N pairs)
+      if (stream_capturing(st))  // overflow records need a host round trip per launch
+        return fail(CFGSIM_ERR_ARG, "allpairs_range: N=" + std::to_string(N) +
+                                        " rows use list kernels, which cannot be captured into a CUDA graph");
       if (S.ovf_cap < w.n_items) {
         CU(cudaStreamSynchronize(st));
         if (int rc = ensure_scratch(S, w.n_items)) return rc;
@@ -1707,7 +1838,10 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
   // overflowed / ambiguous pairs of the per-pair kernels (records hold
   // absolute units); the two-stage path alone needs no host round trip
   if (u_end > u0) {
-    if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
+    // (under capture only large-N kernels ran — list kernels refuse it — and
+    // they leave no overflow records)
+    if (!stream_capturing(st))
+      if (int rc = handle_overflow(c, c, w, p, d_lin, nullptr, iters_lin, nullptr, S, st)) return rc;
     if (int rc = big_status(S, st)) return rc;
   }
   CU(cudaGetLastError());
