@@ -648,10 +648,13 @@ def run_ours(args):
                    for i, m in enumerate(mats)]
             call = lambda: P.pairwise(tms, P.MeasureId.ISO, device=local, precision=args.precision)  # noqa: E731
             api = "paper_1707_02423_b200.pairwise(..., ISO)"
-        res = call()  # warm
+        res = call()  # warm-up: two calls, so both page-locked result buffers the
+        res = call()  # API alternates between (one still held by `res`) exist
+        import gc
         times = []
         for s in range(args.steps):
             flush.fill_(s)
+            gc.collect()  # (outside the timed region: no collector pause lands inside a step)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = call()

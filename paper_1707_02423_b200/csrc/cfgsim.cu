@@ -535,7 +535,7 @@ int big_kcap(double alpha, double tol, int max_iter) {
 
 int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, const PairWork &work,
                const PairOut &out, const cfgsim_params *p, unsigned long long *counter, cudaStream_t st,
-               const double *xg = nullptr, int kg = 0, int convg = 0) {
+               const double *xg = nullptr, int kg = 0, int convg = 0, const BigParams *hist = nullptr) {
   CFGSIM_NVTX("cfgsim.large_n");
   if (nlim > kBigNmax) return fail(CFGSIM_ERR_ARG, "pair size N=" + std::to_string(nlim) + " exceeds 1024");
   const int kb = big_kb(nlim);
@@ -544,6 +544,13 @@ int big_launch(int precision, int nlim, const DevCorpus &A, const DevCorpus &B, 
   prm.xg = xg;  // given-X mode (fp64 only): sort + match an X computed outside
   prm.kg = kg;
   prm.convg = convg;
+  if (hist) {  // history mode (fp64 all-pairs): precomputed per-(graph, N) sequences
+    prm.hu = hist->hu;
+    prm.hd = hist->hd;
+    prm.hstride = hist->hstride;
+    prm.hcbase = hist->hcbase;
+    prm.hapow = hist->hapow;
+  }
   prm.alpha = p->alpha;
   prm.tol = (precision == CFGSIM_FP32) ? std::max(p->tol, p->tol_fp32) : p->tol;
   prm.eps = (precision == CFGSIM_FP32) ? 0.02 : 1e-6;
@@ -779,11 +786,19 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
     return e ? atoi(e) : 3;
   }();
   const int nt = 32 * (pw + 1);
+  const size_t smem = p2_smem_bytes(N, sizeof(T), rr.kcap);
+  // 33 <= N: four CTAs per SM where their shared memory fits (the kernel
+  // compiled for 4 CTAs: <= 102 registers), else three
+  static const int occ4 = [] {  // CFGSIM_P2_OCC4=1 enables (measured neutral: 18.29 vs 18.33 M pairs/s)
+    const char *e = getenv("CFGSIM_P2_OCC4");
+    return e ? atoi(e) : 0;
+  }();
+  const bool four = occ4 && minb_env == 3 && 4 * (smem + 1024) <= (size_t)233472;
   const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
                                           : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
                          : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
+                            : four        ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 4>
                                           : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
-  const size_t smem = p2_smem_bytes(N, sizeof(T), rr.kcap);
   int occ = 0;
   CU(cached_occupancy((const void *)f2, nt, smem, &occ));
   if (occ < 1) return fail(CFGSIM_ERR_CUDA, "stage-2 kernel cannot be resident");
@@ -1708,6 +1723,90 @@ int cfgsim_isorank_pairs(const cfgsim_corpus *A, const cfgsim_corpus *B, int64_t
   return CFGSIM_OK;
 }
 
+namespace {
+// alpha^m by sequential products (the large-N sweeps' ak), m = 0..kmax
+__global__ void big_apow_kernel(double alpha, int kmax, double *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 1.0;
+    for (int m = 0; m <= kmax; m++) {
+      out[m] = a;
+      a *= alpha;
+    }
+  }
+}
+
+int big_hist_min_rows() {  // CFGSIM_BIG_HIST_ROWS: rows a size group needs for history mode
+  static const int v = [] {
+    const char *e = getenv("CFGSIM_BIG_HIST_ROWS");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  return v;
+}
+
+bool use_bighist() {  // CFGSIM_BIG_HIST=0: per-pair sweeps in the large-N kernel (A/B)
+  static const bool on = [] {
+    const char *e = getenv("CFGSIM_BIG_HIST");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+// One size group of large-N rows (rows ra.. of size N) over units [u0, u1):
+// the sequences of every partner graph (sorted positions ra .. K-1) at size
+// N once (isorank_seqbig_kernel), then the pair kernel in history mode.
+// Device-resident tables, no host round trip (capturable).
+int bighist_group(const cfgsim_corpus *c, int ra, int N, int64_t u0, int64_t u1, PairWork w, const PairOut &o,
+                  const cfgsim_params *p, Scratch &S, unsigned long long *ctr, cudaStream_t st) {
+  const int64_t ncombo = c->K - ra;
+  const double tol = p->tol;
+  const int kcap = big_kcap(p->alpha, tol, p->max_iter);
+  const int64_t stride = (int64_t)(kcap + 1) * big_hpitch(N);
+  CU(grow_buf(S.seq_u, sizeof(double) * (size_t)(ncombo * stride), st));
+  CU(grow_buf(S.seq_d, sizeof(double) * (size_t)(ncombo * (kcap + 1)), st));
+  CU(grow_buf(S.seq_apow, sizeof(double) * (size_t)(kcap + 2), st));
+  S.seq_key.clear();  // the shared combo buffers are rewritten
+  big_apow_kernel<<<1, 32, 0, st>>>(p->alpha, kcap + 1, S.seq_apow.as<double>());
+  g_launches++;
+  // stage: the group's sequences
+  BigParams sp{};
+  sp.alpha = p->alpha;
+  sp.tol = tol;
+  sp.eps = 1e-6;
+  sp.max_iter = p->max_iter;
+  sp.kcap = kcap;
+  sp.nlim = N;
+  SeqBigCombos cb{};
+  cb.n = ncombo;
+  cb.N = N;
+  cb.g = c->d_perm + ra;
+  cb.stride = stride;
+  cb.hu = S.seq_u.as<double>();
+  cb.hd = S.seq_d.as<double>();
+  const size_t smem = big_smem_layout<double>(N).total;
+  const void *fk = (const void *)isorank_seqbig_kernel<8>;
+  int dev, sms = 0, occ = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cached_occupancy(fk, BIG_THREADS, smem, &occ));
+  if (occ < 1) return fail(CFGSIM_ERR_CUDA, "sequence kernel cannot be resident");
+  const int64_t grid = std::min<int64_t>((int64_t)sms * occ, ncombo);
+  DevCorpus dc = c->dev();
+  void *args[] = {(void *)&dc, (void *)&cb, (void *)&sp};
+  CU(cudaLaunchKernel(fk, dim3((unsigned)grid), dim3(BIG_THREADS), args, smem, st));
+  g_launches++;
+  // the group's pairs: the large-N kernel in history mode
+  w.u0 = u0;
+  w.n_items = u1 - u0;
+  BigParams hist{};
+  hist.hu = S.seq_u.as<double>();
+  hist.hd = S.seq_d.as<double>();
+  hist.hstride = stride;
+  hist.hcbase = -(int64_t)ra;
+  hist.hapow = S.seq_apow.as<double>();
+  return big_launch(CFGSIM_FP64, N, dc, dc, w, o, p, ctr, st, nullptr, 0, 0, &hist);
+}
+}  // namespace
+
 int cfgsim_allpairs_units(const cfgsim_corpus *c, int64_t *n_units) {
   if (!c || !n_units) return fail(CFGSIM_ERR_ARG, "bad arguments");
   *n_units = c->row_start[c->K];
@@ -1807,7 +1906,43 @@ int cfgsim_allpairs_range(const cfgsim_corpus *c, int64_t u0, int64_t u1, int32_
     w.n_items = seg_end - u;
     w.u0 = u;
     unsigned long long *ctr = S.counters.as<unsigned long long>() + (launch_no % 64);
-    if (big) {
+    if (big && p->precision == CFGSIM_FP64 && !ordered && use_bighist()) {
+      // size groups with many rows share per-(graph, N) sequences (history
+      // mode); runs of small groups go through the per-pair kernel as one
+      // launch (a group's sequences cost about as much as its rows' own
+      // sweeps until it has several rows)
+      int64_t pu0 = -1, pu1 = -1;  // pending per-pair unit range
+      auto flush = [&]() -> int {
+        if (pu1 > pu0 && pu0 >= 0) {
+          PairWork w2 = w;
+          w2.u0 = pu0;
+          w2.n_items = pu1 - pu0;
+          unsigned long long *pctr = S.counters.as<unsigned long long>() + (launch_no++ % 64);
+          const int nl = c->n_sorted[std::upper_bound(c->row_start.begin(), c->row_start.end(), pu0) -
+                                     c->row_start.begin() - 1];
+          if (int rc = big_launch(p->precision, nl, c->dev(), c->dev(), w2, o, p, pctr, st)) return rc;
+        }
+        pu0 = pu1 = -1;
+        return CFGSIM_OK;
+      };
+      for (int ga = a; ga <= a_end;) {
+        int gb = ga;
+        while (gb + 1 <= a_end && c->n_sorted[gb + 1] == c->n_sorted[ga]) gb++;
+        const int64_t gu0 = std::max(u, c->row_start[ga]), gu1 = std::min(seg_end, c->row_start[gb + 1]);
+        if (gu1 > gu0) {
+          if (gb - ga + 1 >= big_hist_min_rows()) {
+            if (int rc = flush()) return rc;
+            unsigned long long *gctr = S.counters.as<unsigned long long>() + (launch_no++ % 64);
+            if (int rc = bighist_group(c, ga, c->n_sorted[ga], gu0, gu1, w, o, p, S, gctr, st)) return rc;
+          } else {
+            if (pu0 < 0) pu0 = gu0;
+            pu1 = gu1;
+          }
+        }
+        ga = gb + 1;
+      }
+      if (int rc = flush()) return rc;
+    } else if (big) {
       if (int rc = big_launch(p->precision, N, c->dev(), c->dev(), w, o, p, ctr, st)) return rc;
     } else {
       // per-pair kernels with operator lists: records of overflowed /

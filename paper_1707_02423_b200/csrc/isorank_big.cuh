@@ -56,7 +56,18 @@ struct BigParams {
   // matches it.  One pair, fp64.
   const double *xg;
   int32_t kg, convg;
+  // history mode (all-pairs, fp64): the sequences u_m of every (graph, N)
+  // come precomputed from isorank_seqbig_kernel (combo of sorted position q
+  // = hcbase + q; rows of pitch big_hpitch(N)), so the pair skips its sweeps
+  const double *hu;
+  const double *hd;      // Du_m per combo, (kcap + 1) each
+  int64_t hstride;       // combo -> offset of its row 0 in hu: combo * hstride
+  int64_t hcbase;
+  const double *hapow;   // alpha^m by sequential products (the sweeps' ak)
 };
+
+// history row pitch (doubles, 16-byte rows)
+__host__ __device__ inline int big_hpitch(int N) { return (N + 1) & ~1; }
 
 // per-CTA global slab
 struct BigSlab {
@@ -397,6 +408,26 @@ __device__ __forceinline__ void big_sort_desc(K (&v)[KB], int lane) {
     }                                                                                 \
   } while (0)
 
+// one side's operator tables in shared memory region `sd` (0 / 1)
+__device__ __forceinline__ void big_side_init(BigSide &S, const DevCorpus &Cs, int g, int N, unsigned char *smem_raw,
+                                              const BigSmem &L, int sd) {
+  S.n = Cs.n_nodes[g];
+  S.N = N;
+  S.kind = (S.n == N) ? 0 : (S.n == 1 ? 2 : 1);
+  S.rp = Cs.rowptr + Cs.rp_off[g];
+  S.cc = Cs.col + Cs.nz_off[g];
+  S.rv = Cs.val + Cs.nz_off[g];
+  S.cp = Cs.cscp + Cs.rp_off[g];
+  S.cr = Cs.csc_row + Cs.nz_off[g];
+  S.cv = Cs.csc_val + Cs.nz_off[g];
+  S.lo = (int16_t *)(smem_raw + L.lo[sd]);
+  S.fr = (double *)(smem_raw + L.fr[sd]);
+  S.rinv = (double *)(smem_raw + L.rinv[sd]);
+  S.pst = (int16_t *)(smem_raw + L.pst[sd]);
+  S.zf = (uint8_t *)(smem_raw + L.zf[sd]);
+  big_build_side(S, (double *)(smem_raw + L.scr));
+}
+
 template <typename T, int KB>
 __global__ void __launch_bounds__(BIG_THREADS, 2)
     isorank_big_kernel(DevCorpus CA, DevCorpus CB, PairWork work, PairOut out, BigParams prm,
@@ -447,26 +478,102 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
           emax = max(emax, x);
         }
       } else {
+      int K = 0;
+      const double invN = 1.0 / (double)N;
+      const double inv_nn = 1.0 / (double)((long long)N * N);
+      const double c = (1.0 - prm.alpha) * inv_nn;  // (1-alpha)*uniform, similarity.py:140
+      const double *hUA = nullptr, *hUB = nullptr;
+      const int HP = big_hpitch(N);
+      if (prm.hu) {
+        // ---- 1-2 (history mode). The stopping sweep from the precomputed
+        // Du_m / Dv_m: every sweep's bracket in parallel, then the exact
+        // delta (the sweeps' formula and reduction, bitwise) only for the
+        // straddling sweeps before the first certain stop, in order
+        BIG_PHASE(0);
+        int pa, pb;
+        {
+          const int64_t u = work.u0 + item;
+          int lo = 0, hi = work.K - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (work.row_start[mid] <= u) lo = mid; else hi = mid - 1;
+          }
+          pa = lo;
+          pb = lo + (int)(u - work.row_start[lo]);
+          if (work.perm[pa] > work.perm[pb]) { const int t = pa; pa = pb; pb = t; }  // side A = lower graph id
+        }
+        const int64_t ca = prm.hcbase + pa, cb = prm.hcbase + pb;
+        hUA = prm.hu + ca * prm.hstride;
+        hUB = prm.hu + cb * prm.hstride;
+        const double *DA = prm.hd + ca * (int64_t)(prm.kcap + 1), *DB = prm.hd + cb * (int64_t)(prm.kcap + 1);
+        int *s_first = (int *)(smem_raw + L.misc + 128);
+        uint32_t *amb = (uint32_t *)(smem_raw + L.misc + 160);  // kcap <= 511
+        const int mmax = prm.max_iter < prm.kcap ? prm.max_iter : prm.kcap;
+        if (tid == 0) *s_first = 0x7fffffff;
+        for (int q = tid; q < 16; q += NT) amb[q] = 0u;
+        __syncthreads();
+        for (int m = tid + 1; m <= mmax; m += NT) {
+          const double ak = prm.hapow[m];
+          const double da = DA[m], db = DB[m];
+          const double hiB = ak * invN * (da + db) * (1.0 + prm.eps);
+          const double loB = ak * invN * fmax(da, db) * (1.0 - prm.eps);
+          if (hiB < prm.tol) atomicMin(s_first, m);
+          else if (loB < prm.tol) atomicOr(amb + (m >> 5), 1u << (m & 31));
+        }
+        __syncthreads();
+        const int first = *s_first;
+        K = mmax;
+        if (first != 0x7fffffff) { K = first; converged = true; }
+        const int lim = first == 0x7fffffff ? mmax : first - 1;
+        for (int wd = 0; wd <= (lim >> 5); wd++) {
+          uint32_t bits = amb[wd];
+          bool done = false;
+          while (bits) {
+            const int m = wd * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (m > lim) break;
+            const double *un = hUA + (size_t)m * HP, *uo = hUA + (size_t)(m - 1) * HP;
+            const double *vn = hUB + (size_t)m * HP, *vo = hUB + (size_t)(m - 1) * HP;
+            double dl = 0.0, dl2 = 0.0;
+            for (int i = warp; i < N; i += BIG_WARPS) {
+              const double a = un[i], b = uo[i];
+              for (int j = lane; j < N; j += 64) {
+                dl += fabs(fma(-b, vo[j], a * vn[j]));
+                if (j + 32 < N) dl2 += fabs(fma(-b, vo[j + 32], a * vn[j + 32]));
+              }
+            }
+            dl += dl2;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dl += __shfl_xor_sync(0xffffffffu, dl, o);
+            __syncthreads();  // (red reused)
+            if (lane == 0) red[warp * 4] = dl;
+            __syncthreads();
+            double Ssum = 0.0;
+            for (int w = 0; w < BIG_WARPS; w++) Ssum += red[w * 4];
+            if (prm.hapow[m] * inv_nn * Ssum < prm.tol) {  // similarity.py:144
+              K = m;
+              converged = true;
+              done = true;
+              break;
+            }
+          }
+          if (done) break;
+        }
+        it_done = converged ? K : prm.max_iter;
+        if (!converged && prm.max_iter > prm.kcap) {  // cannot happen: the bracket stops by kcap
+          if (tid == 0) {
+            atomicExch(prm.status, 1);
+            if (out.iters) out.iters[slot] = -2;
+          }
+          __syncthreads();
+          continue;
+        }
+        __syncthreads();
+      } else {
       BIG_PHASE(0);
       // ---- 1. operators
       BigSide SA, SB;
-      auto setup = [&](BigSide &S, const DevCorpus &Cs, int g, int sd) {
-        S.n = Cs.n_nodes[g];
-        S.N = N;
-        S.kind = (S.n == N) ? 0 : (S.n == 1 ? 2 : 1);
-        S.rp = Cs.rowptr + Cs.rp_off[g];
-        S.cc = Cs.col + Cs.nz_off[g];
-        S.rv = Cs.val + Cs.nz_off[g];
-        S.cp = Cs.cscp + Cs.rp_off[g];
-        S.cr = Cs.csc_row + Cs.nz_off[g];
-        S.cv = Cs.csc_val + Cs.nz_off[g];
-        S.lo = (int16_t *)(smem_raw + L.lo[sd]);
-        S.fr = (double *)(smem_raw + L.fr[sd]);
-        S.rinv = (double *)(smem_raw + L.rinv[sd]);
-        S.pst = (int16_t *)(smem_raw + L.pst[sd]);
-        S.zf = (uint8_t *)(smem_raw + L.zf[sd]);
-        big_build_side(S, (double *)(smem_raw + L.scr));
-      };
+      auto setup = [&](BigSide &S, const DevCorpus &Cs, int g, int sd) { big_side_init(S, Cs, g, N, smem_raw, L, sd); };
       setup(SA, C1, g1, 0);
       setup(SB, C2, g2, 1);
       T *ring[2] = {(T *)(smem_raw + L.ring[0]), (T *)(smem_raw + L.ring[1])};
@@ -483,9 +590,6 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         Vh[q] = (T)1;
       }
       double zsum[2] = {SA.zcount, SB.zcount};
-      const double invN = 1.0 / (double)N;
-      const double inv_nn = 1.0 / (double)((long long)N * N);
-      const double c = (1.0 - prm.alpha) * inv_nn;  // (1-alpha)*uniform, similarity.py:140
       double ak1 = 1.0;                             // alpha^(k-1)
       int k = 1;
       __syncthreads();
@@ -517,24 +621,25 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         // phase 2: u_k = W t + zsum/N; partial sums of |u_k - u_{k-1}| and z^T u_k
         double part[4] = {0.0, 0.0, 0.0, 0.0};
         {
+          // (each side with the same thread mapping, q = tid + NT j, as the
+          // per-(graph, N) history kernel: identical per-thread partial sums,
+          // hence bitwise-identical sequences on both paths)
           const double za = zsum[0] * invN, zb = zsum[1] * invN;
-          for (int q = tid; q < 2 * N; q += NT) {
-            if (q < N) {
-              const T un = big_u_entry<T>(SA, tv[0], q, za);
-              const T uo = ring[0][cur * N + q];
-              ring[0][nxt * N + q] = un;
-              if (k <= prm.kcap) Uh[(size_t)k * N + q] = un;
-              part[0] += fabs((double)un - (double)uo);
-              if (SA.zf[q]) part[1] += (double)un;
-            } else {
-              const int i = q - N;
-              const T un = big_u_entry<T>(SB, tv[1], i, zb);
-              const T uo = ring[1][cur * N + i];
-              ring[1][nxt * N + i] = un;
-              if (k <= prm.kcap) Vh[(size_t)k * N + i] = un;
-              part[2] += fabs((double)un - (double)uo);
-              if (SB.zf[i]) part[3] += (double)un;
-            }
+          for (int q = tid; q < N; q += NT) {
+            const T un = big_u_entry<T>(SA, tv[0], q, za);
+            const T uo = ring[0][cur * N + q];
+            ring[0][nxt * N + q] = un;
+            if (k <= prm.kcap) Uh[(size_t)k * N + q] = un;
+            part[0] += fabs((double)un - (double)uo);
+            if (SA.zf[q]) part[1] += (double)un;
+          }
+          for (int i = tid; i < N; i += NT) {
+            const T un = big_u_entry<T>(SB, tv[1], i, zb);
+            const T uo = ring[1][cur * N + i];
+            ring[1][nxt * N + i] = un;
+            if (k <= prm.kcap) Vh[(size_t)k * N + i] = un;
+            part[2] += fabs((double)un - (double)uo);
+            if (SB.zf[i]) part[3] += (double)un;
           }
         }
 #pragma unroll
@@ -590,7 +695,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         if (k >= prm.max_iter) break;
         ak1 = ak;
       }
-      const int K = k;  // x after K sweeps (similarity.py:139-148)
+      K = k;  // x after K sweeps (similarity.py:139-148)
       if (K > prm.kcap) {  // cannot happen: the bracket stops by kcap
         if (tid == 0) {
           atomicExch(prm.status, 1);
@@ -599,6 +704,7 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         __syncthreads();
         continue;
       }
+      }  // (sweeps)
       // coefficients: c alpha^m (m < K), alpha^K / N^2 (m = K)
       if (tid == 0) {
         double a = 1.0;
@@ -616,7 +722,15 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
       //         exponent range of X for the pair-wide sort keys.
       //         u_m is pre-scaled by coef_m in place (the product the
       //         low-rank kernel forms as cak * u).
-      for (int e = tid; e < (K + 1) * N; e += NT) Uh[e] = coef[e / N] * Uh[e];
+      if (prm.hu) {  // the product's operands from the histories: coef_m u_m, v_m (pitch N)
+        for (int e = tid; e < (K + 1) * N; e += NT) {
+          const int m = e / N, i = e - m * N;
+          Uh[e] = coef[m] * (T)hUA[(size_t)m * HP + i];
+          Vh[e] = (T)hUB[(size_t)m * HP + i];
+        }
+      } else {
+        for (int e = tid; e < (K + 1) * N; e += NT) Uh[e] = coef[e / N] * Uh[e];
+      }
       __syncthreads();
       {
         T *Us = (T *)(smem_raw + L.us);
@@ -1056,6 +1170,90 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
         for (int e = tid; e < N * N; e += NT) out.X[e] = (double)X[e];
       __syncthreads();
     }
+  }
+}
+
+// Per-(graph, N) sequences for the history mode of the large-N kernel: one
+// CTA per combo (grid-stride), the side's operator exactly as the pair kernel
+// builds it, kcap sweeps with the pair kernel's per-side arithmetic and
+// thread mapping (bitwise the same u_m and Du_m), rows stored at pitch
+// big_hpitch(N).  A size group of the triangle (rows a with n_a = N) shares
+// the sequences of every partner graph, so each sequence is computed once
+// per group instead of once per pair.
+struct SeqBigCombos {
+  int64_t n;
+  int32_t N;
+  const int32_t *g;     // combo -> graph (the size-sorted permutation from the group's first row)
+  int64_t stride;       // combo -> offset of row 0: combo * stride
+  double *hu;
+  double *hd;           // (kcap + 1) per combo
+};
+
+template <int KB>
+__global__ void __launch_bounds__(BIG_THREADS, 2)
+    isorank_seqbig_kernel(DevCorpus C, SeqBigCombos cb, BigParams prm) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const BigSmem L = big_smem_layout<double>(prm.nlim);
+  double *red = (double *)(smem_raw + L.red);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = BIG_THREADS;
+  const int N = cb.N, HP = big_hpitch(N);
+  const double invN = 1.0 / (double)N;
+  for (int64_t c = blockIdx.x; c < cb.n; c += gridDim.x) {
+    BigSide S;
+    big_side_init(S, C, cb.g[c], N, smem_raw, L, 0);
+    double *ring = (double *)(smem_raw + L.ring[0]);
+    double *tv = (double *)(smem_raw + L.t[0]);
+    double *sbuf = (double *)(smem_raw + L.scr);
+    double *U = cb.hu + c * cb.stride;
+    double *D = cb.hd + c * (int64_t)(prm.kcap + 1);
+    for (int q = tid; q < N; q += NT) {
+      ring[q] = 1.0;
+      U[q] = 1.0;
+    }
+    if (tid == 0) D[0] = 0.0;
+    double zsum = S.zcount;
+    __syncthreads();
+    for (int k = 1; k <= prm.kcap; k++) {
+      const int cur = (k - 1) & 1, nxt = k & 1;
+      const int n0 = S.kind == 2 ? 0 : S.n;
+      if (S.kind == 1) {
+        for (int q = tid; q < S.n; q += NT) sbuf[q] = big_s_entry<double>(S, ring + cur * N, q);
+        __syncthreads();
+      }
+      for (int q = tid; q < n0; q += NT)
+        tv[q] = S.kind == 1 ? big_t_from_s<double>(S, sbuf, q) : big_t_entry<double>(S, ring + cur * N, q);
+      __syncthreads();
+      double part[2] = {0.0, 0.0};
+      const double z = zsum * invN;
+      for (int q = tid; q < N; q += NT) {
+        const double un = big_u_entry<double>(S, tv, q, z);
+        const double uo = ring[cur * N + q];
+        ring[nxt * N + q] = un;
+        U[(size_t)k * HP + q] = un;
+        part[0] += fabs(un - uo);
+        if (S.zf[q]) part[1] += un;
+      }
+#pragma unroll
+      for (int v = 0; v < 2; v++) {
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) part[v] += __shfl_xor_sync(0xffffffffu, part[v], m);
+      }
+      double *rb = red + (k & 1) * BIG_WARPS * 4;
+      if (lane == 0) {
+        rb[warp * 4] = part[0];
+        rb[warp * 4 + 1] = part[1];
+      }
+      __syncthreads();
+      double tot[2] = {0.0, 0.0};
+      for (int w = 0; w < BIG_WARPS; w++) {
+        tot[0] += rb[w * 4];
+        tot[1] += rb[w * 4 + 1];
+      }
+      zsum = tot[1];
+      if (tid == 0) D[k] = tot[0];
+    }
+    __syncthreads();  // smem tables are rebuilt for the next combo
   }
 }
 

@@ -3,3 +3,4 @@
 #include "tiers.h"
 
 CFGSIM_BIG_LIST_T(double, CFGSIM_INSTANTIATE_BIG)
+template __global__ void cfgsim::isorank_seqbig_kernel<8>(cfgsim::DevCorpus, cfgsim::SeqBigCombos, cfgsim::BigParams);
