@@ -787,17 +787,9 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
   }();
   const int nt = 32 * (pw + 1);
   const size_t smem = p2_smem_bytes(N, sizeof(T), rr.kcap);
-  // 33 <= N: four CTAs per SM where their shared memory fits (the kernel
-  // compiled for 4 CTAs: <= 102 registers), else three
-  static const int occ4 = [] {  // CFGSIM_P2_OCC4=1 enables (measured neutral: 18.29 vs 18.33 M pairs/s)
-    const char *e = getenv("CFGSIM_P2_OCC4");
-    return e ? atoi(e) : 0;
-  }();
-  const bool four = occ4 && minb_env == 3 && 4 * (smem + 1024) <= (size_t)233472;
   const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
                                           : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
                          : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
-                            : four        ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 4>
                                           : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
   int occ = 0;
   CU(cached_occupancy((const void *)f2, nt, smem, &occ));
