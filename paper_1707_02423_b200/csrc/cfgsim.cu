@@ -7,6 +7,7 @@
 // persistent kernels that pull pairs from an atomic work counter (pair cost
 // varies ~8x with the data-dependent iteration count).
 #include <cuda_runtime.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <condition_variable>
@@ -821,12 +822,13 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
     CU(cudaMemcpyAsync(ph, pp.phase, sizeof(ph), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     double tp = 0, tc = 0;
-    for (int k = 0; k < 5; k++) tp += (double)ph[k];
+    for (int k = 0; k < 6; k++) tp += (double)ph[k];
     for (int k = 8; k < 10; k++) tc += (double)ph[k];
     fprintf(stderr, "[cfgsim pair2 N=%d items=%lld grid=%lld] producer: wait/claim %.1f%% bracket+delta %.1f%% "
             "stage+mma+keys %.1f%% row-orders %.1f%% tail %.1f%% (%.3e cyc) | consumer: wait %.1f%% rounds %.1f%% "
-            "(%.3e cyc)\n", N, (long long)w.n_items, (long long)grid, 100 * ph[0] / tp, 100 * ph[1] / tp,
-            100 * ph[2] / tp, 100 * ph[3] / tp, 100 * ph[4] / tp, tp, 100 * ph[8] / tc, 100 * ph[9] / tc, tc);
+            "(%.3e cyc) | of which keys %.1f%%\n", N, (long long)w.n_items, (long long)grid, 100 * ph[0] / tp,
+            100 * ph[1] / tp, 100 * (ph[2] + ph[5]) / tp, 100 * ph[3] / tp, 100 * ph[4] / tp, tp, 100 * ph[8] / tc,
+            100 * ph[9] / tc, tc, 100 * ph[5] / tp);
   }
   return CFGSIM_OK;
 }
@@ -1377,8 +1379,15 @@ class HostPool {
 
  private:
   HostPool() {
-    const char *e = getenv("CFGSIM_HOST_THREADS");  // host packing threads (default: all cores, <= 32)
-    const int n = e && atoi(e) > 0 ? atoi(e) : std::min(32, (int)std::thread::hardware_concurrency());
+    // host packing threads (CFGSIM_HOST_THREADS; default: the CPUs this
+    // process may run on, at most 8 — packing a corpus is a few ms of work,
+    // and a burst of more threads than the container's CPU quota gets the
+    // whole process throttled for a scheduler period)
+    const char *e = getenv("CFGSIM_HOST_THREADS");
+    int avail = (int)std::thread::hardware_concurrency();
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) avail = CPU_COUNT(&set);
+    const int n = e && atoi(e) > 0 ? atoi(e) : std::max(1, std::min(8, avail));
     for (int t = 1; t < n; t++) th_.emplace_back([this] { loop(); });
   }
   void loop() {

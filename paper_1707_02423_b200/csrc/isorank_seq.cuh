@@ -1024,6 +1024,7 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
                            : "d"(af[x]), "d"(bf[y]));
         }
       }
+      P2_PHASE(5);  // exponent range + key build
       big_cp_async_wait_group<0>();  // (only empty groups remain; the producer barrier below the
                                      // exponent reduction orders the key writes after every read)
 #pragma unroll
