@@ -904,34 +904,55 @@ int seq_nearest_t(const cfgsim_corpus *Q, const cfgsim_corpus *C, const std::vec
                          : std::lower_bound(v.begin(), v.end(), n, [&](int x, int t) { return X->n_nodes[x] < t; })) -
                      v.begin());
   };
-  for (int N : ns) {
+  // every size's rectangles and their prefix sums, uploaded once (no host
+  // synchronisation between the sizes: the combo tables of the next size are
+  // rewritten in stream order after the previous size's kernels)
+  std::vector<int32_t> all_rects;
+  std::vector<int64_t> all_rsum;
+  std::vector<size_t> at_rect(ns.size()), at_rsum(ns.size());
+  std::vector<int> nrs(ns.size(), 0);
+  for (size_t gi = 0; gi < ns.size(); gi++) {
+    const int N = ns[gi];
     const int32_t qlt = cnt(qs, Q, N, false), qle = cnt(qs, Q, N, true);
     const int32_t clt = cnt(cs, C, N, false), cle = cnt(cs, C, N, true);
-    std::vector<int32_t> rects;
-    if (qle > qlt && cle > 0) rects.insert(rects.end(), {qlt, qle, 0, cle});
-    if (qlt > 0 && cle > clt) rects.insert(rects.end(), {0, qlt, clt, cle});
-    if (rects.empty()) continue;
+    at_rect[gi] = all_rects.size();
+    at_rsum[gi] = all_rsum.size();
+    if (qle > qlt && cle > 0) all_rects.insert(all_rects.end(), {qlt, qle, 0, cle});
+    if (qlt > 0 && cle > clt) all_rects.insert(all_rects.end(), {0, qlt, clt, cle});
+    const int nr = (int)(all_rects.size() - at_rect[gi]) / 4;
+    nrs[gi] = nr;
+    int64_t acc = 0;
+    all_rsum.push_back(0);
+    for (int r = 0; r < nr; r++) {
+      const int32_t *R = all_rects.data() + at_rect[gi] + 4 * r;
+      acc += (int64_t)(R[1] - R[0]) * (R[3] - R[2]);
+      all_rsum.push_back(acc);
+    }
+  }
+  DBuf drs, drect;
+  CU(drs.alloc(sizeof(int64_t) * std::max<size_t>(all_rsum.size(), 1)));
+  CU(drect.alloc(sizeof(int32_t) * std::max<size_t>(all_rects.size(), 1)));
+  if (!all_rsum.empty())
+    CU(cudaMemcpyAsync(drs.p, all_rsum.data(), sizeof(int64_t) * all_rsum.size(), cudaMemcpyHostToDevice, st));
+  if (!all_rects.empty())
+    CU(cudaMemcpyAsync(drect.p, all_rects.data(), sizeof(int32_t) * all_rects.size(), cudaMemcpyHostToDevice, st));
+  for (size_t gi = 0; gi < ns.size(); gi++) {
+    const int N = ns[gi];
+    const int nr = nrs[gi];
+    if (nr == 0) continue;
+    const int32_t qle = cnt(qs, Q, N, true), cle = cnt(cs, C, N, true);
     SeqTable tb;  // [queries with n <= N | corpus graphs with n <= N], sorted positions
     for (int32_t q = 0; q < qle; q++) tb.add<T>(qs[q], N, rr.kcap);
     for (int32_t x = 0; x < cle; x++) tb.add<T>(cs[x], N, rr.kcap);
     if (int rc = seq_upload<T>(S, tb, rr, p, st)) return rc;
     if (int rc = seq_stage1<T>(Q, 0, qle, rr, p, S, st)) return rc;
     if (int rc = seq_stage1<T>(C, qle, cle, rr, p, S, st)) return rc;
-    const int nr = (int)rects.size() / 4;
-    std::vector<int64_t> rsum(nr + 1, 0);
-    for (int r = 0; r < nr; r++)
-      rsum[r + 1] = rsum[r] + (int64_t)(rects[4 * r + 1] - rects[4 * r]) * (rects[4 * r + 3] - rects[4 * r + 2]);
-    DBuf drs, drect;
-    CU(drs.alloc(sizeof(int64_t) * (nr + 1)));
-    CU(drect.alloc(sizeof(int32_t) * 4 * nr));
-    CU(cudaMemcpyAsync(drs.p, rsum.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(drect.p, rects.data(), sizeof(int32_t) * 4 * nr, cudaMemcpyHostToDevice, st));
     PairWork w{};
     w.mode = WORK_RECT;
-    w.n_items = rsum[nr];
+    w.n_items = all_rsum[at_rsum[gi] + nr];
     w.nrect = nr;
-    w.rect_start = drs.as<int64_t>();
-    w.rect = drect.as<int32_t>();
+    w.rect_start = drs.as<int64_t>() + at_rsum[gi];
+    w.rect = drect.as<int32_t>() + at_rect[gi];
     w.qperm = dqs;
     w.cperm = dcs;
     w.qbase = q0;
@@ -940,8 +961,8 @@ int seq_nearest_t(const cfgsim_corpus *Q, const cfgsim_corpus *C, const std::vec
     PairOut o{};
     o.d = dm;
     if (int rc = seq_stage2<T>(N, 0, qle, w, o, rr, p, S, launch_no, st)) return rc;
-    CU(cudaStreamSynchronize(st));  // drs / drect and the combo buffers are reused by the next N
   }
+  CU(cudaStreamSynchronize(st));  // (drs / drect are freed on return)
   return CFGSIM_OK;
 }
 
