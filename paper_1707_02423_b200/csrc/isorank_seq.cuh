@@ -636,27 +636,18 @@ __device__ __forceinline__ void p2_row_order_pair(const unsigned long long *Krow
                                                   bool act) {
   constexpr int VB = sizeof(T) == 8 ? 58 : 31;
   uint32_t v[32];
+  // half 1 sorts the complemented keys descending, i.e. its keys ascending:
+  // one compile-time network for both halves (no per-exchange direction select)
+  const uint32_t flip = half ? 0xffffffffu : 0u;
 #pragma unroll
   for (int q = 0; q < 32; q++) {
     const int j = half * 32 + q;
-    v[q] = (act && j < N) ? (uint32_t)((((Krow[j] >> 6) >> (VB - 26)) << 6) | (Krow[j] & 63ull)) : 0u;
+    v[q] = ((act && j < N) ? (uint32_t)((((Krow[j] >> 6) >> (VB - 26)) << 6) | (Krow[j] & 63ull)) : 0u) ^ flip;
   }
   // sort half 0 descending, half 1 ascending (padding 0 ends up last overall)
+  p2_sort_u32<1>(v);
 #pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-      for (int i = 0; i < 32; i++) {
-        const int l = i ^ j;
-        if (l > i) {
-          const uint32_t a = v[i], b = v[l];
-          const uint32_t hi = max(a, b), lo = min(a, b);
-          const bool desc = ((i & k) == 0) == (half == 0);
-          v[i] = desc ? hi : lo;
-          v[l] = desc ? lo : hi;
-        }
-      }
+  for (int q = 0; q < 32; q++) v[q] ^= flip;
 #pragma unroll
   for (int q = 0; q < 32; q++) {  // half 0 keeps the larger 32, half 1 the smaller
     const uint32_t o = __shfl_xor_sync(0xffffffffu, v[q], 1);
