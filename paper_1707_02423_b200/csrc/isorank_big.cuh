@@ -346,30 +346,33 @@ __device__ __forceinline__ void big_cp_async_commit() { asm volatile("cp.async.c
 template <int G>
 __device__ __forceinline__ void big_cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(G) : "memory"); }
 
-// compare-exchange of registers c and c ^ J inside each lane (elements
-// e = lane * KB + c), direction by bit k of e
+// compare-exchange of registers c and c ^ J inside each lane, larger key to
+// the lower register (every block descending: see big_sort_desc)
 template <typename K, int KB, int J>
-__device__ __forceinline__ void big_stage_reg(K (&v)[KB], int lane, int k) {
+__device__ __forceinline__ void big_stage_reg(K (&v)[KB]) {
 #pragma unroll
   for (int c = 0; c < KB; c++) {
     if ((c & J) == 0) {
-      const int pc = c | J;
-      const bool up = (((lane * KB + c) & k) == 0);
-      const K a = v[c], b = v[pc];
-      const K hi = a > b ? a : b, lo = a > b ? b : a;
-      v[c] = up ? hi : lo;
-      v[pc] = up ? lo : hi;
+      const K a = v[c], b = v[c | J];
+      v[c] = a > b ? a : b;
+      v[c | J] = a > b ? b : a;
     }
   }
 }
 
 // Warp bitonic sort of 32*KB distinct keys, descending; element e = lane*KB + c
 // (each lane holds a contiguous run, so only log2(32) of every merge's stages
-// cross lanes).  Stage loops stay rolled: the fully unrolled 1024-key network
-// does not fit the instruction cache.
+// cross lanes).  During merge level k the blocks with bit k of e set sort
+// ascending; they hold their keys complemented (~key), so every
+// compare-exchange runs descending with no per-exchange direction select, and
+// one xor per key re-targets the complement between levels.  Stage loops stay
+// rolled: the fully unrolled 1024-key network does not fit the instruction cache.
 template <typename K, int KB>
 __device__ __forceinline__ void big_sort_desc(K (&v)[KB], int lane) {
   constexpr int n = 32 * KB;
+  auto flip = [&](int c, int k) -> K { return (((lane * KB + c) & k) != 0) ? ~K(0) : K(0); };
+#pragma unroll
+  for (int c = 0; c < KB; c++) v[c] ^= flip(c, 2);
 #pragma unroll 1
   for (int k = 2; k <= n; k <<= 1) {
 #pragma unroll 1
@@ -380,20 +383,22 @@ __device__ __forceinline__ void big_sort_desc(K (&v)[KB], int lane) {
 #pragma unroll
         for (int c = 0; c < KB; c++) {
           const K o = __shfl_xor_sync(0xffffffffu, v[c], lm);
-          const bool up = (((lane * KB + c) & k) == 0);
-          const K hi = o > v[c] ? o : v[c], lo = o > v[c] ? v[c] : o;
-          v[c] = (lower == up) ? hi : lo;
+          v[c] = lower ? (o > v[c] ? o : v[c]) : (o > v[c] ? v[c] : o);
         }
       } else {
         switch (j) {
-          case 1: big_stage_reg<K, KB, 1>(v, lane, k); break;
-          case 2: if constexpr (KB > 2) big_stage_reg<K, KB, 2>(v, lane, k); break;
-          case 4: if constexpr (KB > 4) big_stage_reg<K, KB, 4>(v, lane, k); break;
-          case 8: if constexpr (KB > 8) big_stage_reg<K, KB, 8>(v, lane, k); break;
-          case 16: if constexpr (KB > 16) big_stage_reg<K, KB, 16>(v, lane, k); break;
+          case 1: big_stage_reg<K, KB, 1>(v); break;
+          case 2: if constexpr (KB > 2) big_stage_reg<K, KB, 2>(v); break;
+          case 4: if constexpr (KB > 4) big_stage_reg<K, KB, 4>(v); break;
+          case 8: if constexpr (KB > 8) big_stage_reg<K, KB, 8>(v); break;
+          case 16: if constexpr (KB > 16) big_stage_reg<K, KB, 16>(v); break;
           default: break;
         }
       }
+    }
+    if (k < n) {  // level 2k's complement (bit k of e ends up 0 at the last level)
+#pragma unroll
+      for (int c = 0; c < KB; c++) v[c] ^= flip(c, k) ^ flip(c, 2 * k);
     }
   }
 }
