@@ -10,6 +10,7 @@ the partner's size, so it happens per pair inside the kernel prologue.
 
 from __future__ import annotations
 
+import ctypes
 from typing import Sequence
 
 import numpy as np
@@ -17,6 +18,25 @@ import numpy as np
 from . import _native as nat
 from .packing import _entries, pack, packed_bytes  # noqa: F401  (re-exported)
 
+
+
+_read_ptr = ctypes.c_void_p.from_address
+_DATA_OFFSET = 16  # PyArrayObject: PyObject_HEAD (refcount, type), then `char *data`
+
+
+def _data_pointers(arrays: list) -> list:
+    """Data addresses of ndarrays, read from each array object's `data` field
+    (numpy's C ABI, PyArrayObject_fields) — ~5x cheaper per array than
+    ``a.ctypes.data``, which matters on the per-call path of a 2k-matrix
+    corpus.  Checked against ``__array_interface__`` on the first and last
+    array; any mismatch falls back to the interface for every array."""
+    if not arrays:
+        return []
+    ptrs = [_read_ptr(id(a) + _DATA_OFFSET).value for a in arrays]
+    if (ptrs[0] != arrays[0].__array_interface__["data"][0]
+            or ptrs[-1] != arrays[-1].__array_interface__["data"][0]):
+        ptrs = [a.__array_interface__["data"][0] for a in arrays]
+    return ptrs
 
 
 class DeviceCorpus:
@@ -40,7 +60,7 @@ class DeviceCorpus:
                     raise ValueError(f"matrix {g}: entries must be square and non-empty, got {e.shape}")
             self.n_nodes = np.array([e.shape[0] for e in es], np.int32)
             self.K = len(es)
-            ptrs = (nat.C.c_void_p * self.K)(*[e.ctypes.data for e in es])
+            ptrs = (nat.C.c_void_p * self.K)(*_data_pointers(es))
             nat.check(nat.lib.cfgsim_corpus_create_dense(self.device, self.K, nat.ptr(self.n_nodes), ptrs,
                                                          nat.C.byref(h)))
         self._h = h

@@ -791,6 +791,7 @@ int seq_stage2(int N, int64_t cbase, int64_t cbase2, const PairWork &w, const Pa
   const void *f2 = small ? (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 4>
                                           : (const void *)isorank_pair2_kernel<T, 1, 4, 4, 2, 6>)
                          : (minb_env == 2 ? (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 2>
+                            : N <= 48     ? (const void *)isorank_pair2_kernel<T, 2, 4, 6, 4, 3>  // 6 x 6 mma tiles
                                           : (const void *)isorank_pair2_kernel<T, 2, 4, 8, 4, 3>);
   int occ = 0;
   CU(cached_occupancy((const void *)f2, nt, smem, &occ));

@@ -381,6 +381,10 @@ __host__ __device__ inline int p2_stage_pitch(int npt, int tsize) {
   return tsize == 8 ? ((2 * npt + 11) / 16) * 16 + 4 : ((2 * npt + 7) / 16) * 16 + 8;
 }
 
+// row-order pitch (bytes): rows start 4-byte aligned so the orders are
+// written as packed 32-bit words
+__host__ __device__ inline int p2_ord_pitch(int N) { return (N + 3) & ~3; }
+
 __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
   P2Smem s;
   size_t o = 0;
@@ -396,7 +400,7 @@ __host__ __device__ inline P2Smem p2_smem_layout(int N, int tsize, int kcap) {
   if (kb > xb) xb = kb;
   for (int q = 0; q < 2; q++) {
     s.x[q] = take(xb > sb ? xb : sb);  // X_K (aliases the u/v staging while it is built)
-    s.ord[q] = take((size_t)N * N);    // row orders (columns, value desc / column asc)
+    s.ord[q] = take((size_t)N * p2_ord_pitch(N));  // row orders (columns, value desc / column asc)
   }
   s.meta = take(2 * sizeof(P2Meta));
   s.red = take(8 * sizeof(double));  // one partial per producer warp
@@ -484,6 +488,7 @@ __device__ __forceinline__ void p2_sort_row(const T *row, int N, uint8_t *ord, i
 // (row-order sum), mrow[i] = matched column.
 template <typename T, int KB>
 __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uint8_t *ord, int32_t *mrow, int lane) {
+  const int OP = p2_ord_pitch(N);
   int ptr[KB], ccol[KB];
   T cur[KB];
   bool act[KB];
@@ -494,7 +499,7 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
     act[cc] = i < N;
     ptr[cc] = 0;
     taken[cc] = 0u;
-    ccol[cc] = act[cc] ? (int)ord[i * N] : 0;
+    ccol[cc] = act[cc] ? (int)ord[i * OP] : 0;
     cur[cc] = act[cc] ? Xs[i * P + ccol[cc]] : (T)-3;
   }
   for (int round = 0; round < N; round++) {
@@ -527,7 +532,7 @@ __device__ __forceinline__ double p2_rounds(const T *Xs, int P, int N, const uin
         bool tk;
         do {
           ++p;
-          col = ord[i * N + p];
+          col = ord[i * OP + p];
           uint32_t word = 0;
 #pragma unroll
           for (int q = 0; q < KB; q++)
@@ -606,13 +611,24 @@ __device__ __forceinline__ void p2_row_order(const unsigned long long *Krow, int
   for (int q = 0; q < 32 * KB; q++)
     v[q] = (q < N) ? (uint32_t)((((Krow[q] >> 6) >> (VB - 26)) << 6) | (Krow[q] & 63ull)) : 0u;  // padding last
   p2_sort_u32<KB>(v);
-  bool coll = false;
+  // orders as packed 32-bit words (ord is 4-byte aligned, pitch p2_ord_pitch)
 #pragma unroll
-  for (int q = 0; q < 32 * KB; q++) {
-    if (q < N) ord[q] = (uint8_t)(63 - (int)(v[q] & 63u));
-    if (q + 1 < 32 * KB && q + 1 < N && (v[q] >> 6) == (v[q + 1] >> 6) &&
-        (Krow[63 - (v[q] & 63u)] >> 6) != (Krow[63 - (v[q + 1] & 63u)] >> 6))
-      coll = true;
+  for (int w = 0; w < 8 * KB; w++)
+    if (4 * w < N)
+      reinterpret_cast<uint32_t *>(ord)[w] = (63u - (v[4 * w] & 63u)) | ((63u - (v[4 * w + 1] & 63u)) << 8) |
+                                              ((63u - (v[4 * w + 2] & 63u)) << 16) | ((63u - (v[4 * w + 3] & 63u)) << 24);
+  // neighbours with equal 26-bit prefixes are looked up exactly (no key loads
+  // unless some prefix ties)
+  uint32_t tie = 0u;
+#pragma unroll
+  for (int q = 0; q + 1 < 32 * KB; q++)
+    if (q + 1 < N && (v[q] >> 6) == (v[q + 1] >> 6)) tie |= 1u << (q & 31);
+  bool coll = false;
+  if (tie) {
+#pragma unroll
+    for (int q = 0; q + 1 < 32 * KB; q++)
+      if (((tie >> (q & 31)) & 1u) && (Krow[63 - (v[q] & 63u)] >> 6) != (Krow[63 - (v[q + 1] & 63u)] >> 6))
+        coll = true;
   }
   if (coll) {
     for (int p = 1; p < N; p++) {
@@ -664,19 +680,32 @@ __device__ __forceinline__ void p2_row_order_pair(const unsigned long long *Krow
         v[l] = min(a, b);
       }
     }
-  bool coll = false;
+  // orders as packed 32-bit words (rows 4-byte aligned at pitch
+  // p2_ord_pitch(N) >= N: a word starting below N stays inside the row)
+#pragma unroll
+  for (int w = 0; w < 8; w++)
+    if (act && half * 32 + 4 * w < N)
+      reinterpret_cast<uint32_t *>(ord + half * 32)[w] =
+          (63u - (v[4 * w] & 63u)) | ((63u - (v[4 * w + 1] & 63u)) << 8) | ((63u - (v[4 * w + 2] & 63u)) << 16) |
+          ((63u - (v[4 * w + 3] & 63u)) << 24);
+  // neighbours with equal 26-bit prefixes are looked up exactly (no key loads
+  // unless some prefix ties)
+  const uint32_t first1 = __shfl_down_sync(0xffffffffu, v[0], 1);  // half 1's first, seen by half 0
+  uint32_t tie = 0u;
 #pragma unroll
   for (int q = 0; q < 32; q++) {
-    const int pos = half * 32 + q;
-    if (act && pos < N) ord[pos] = (uint8_t)(63 - (int)(v[q] & 63u));
-    if (q + 1 < 32 && act && pos + 1 < N && (v[q] >> 6) == (v[q + 1] >> 6) &&
-        (Krow[63 - (v[q] & 63u)] >> 6) != (Krow[63 - (v[q + 1] & 63u)] >> 6))
-      coll = true;
+    const uint32_t nx = q + 1 < 32 ? v[q + 1] : first1;
+    const bool in = q + 1 < 32 ? half * 32 + q + 1 < N : (half == 0 && 32 < N);
+    if (act && in && (v[q] >> 6) == (nx >> 6)) tie |= 1u << q;
   }
-  const uint32_t first1 = __shfl_down_sync(0xffffffffu, v[0], 1);  // half 1's first, seen by half 0
-  if (half == 0 && act && 32 < N && (v[31] >> 6) == (first1 >> 6) &&
-      (Krow[63 - (v[31] & 63u)] >> 6) != (Krow[63 - (first1 & 63u)] >> 6))
-    coll = true;
+  bool coll = false;
+  if (tie) {
+#pragma unroll
+    for (int q = 0; q < 32; q++) {
+      const uint32_t nx = q + 1 < 32 ? v[q + 1] : first1;
+      if (((tie >> q) & 1u) && (Krow[63 - (v[q] & 63u)] >> 6) != (Krow[63 - (nx & 63u)] >> 6)) coll = true;
+    }
+  }
   const int other = __shfl_xor_sync(0xffffffffu, coll ? 1 : 0, 1);  // (unconditional: every lane shuffles)
   coll = coll || other != 0;
   __syncwarp();
@@ -704,6 +733,7 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
   int ptr[KB];
   bool act[KB];
   uint32_t tk[KB];  // taken columns, 32 per word (32-bit tests on the advance path)
+  const int OP = p2_ord_pitch(N);
 #pragma unroll
   for (int q = 0; q < KB; q++) tk[q] = 0u;
   auto taken_col = [&](int c) { return ((KB > 1 && c >= 32 ? tk[KB - 1] : tk[0]) >> (c & 31)) & 1u; };
@@ -712,7 +742,7 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
     const int i = lane + 32 * cc;
     act[cc] = i < N;
     ptr[cc] = 0;
-    hk[cc] = act[cc] ? Kr[i * PK + ord[i * N]] : 0ull;
+    hk[cc] = act[cc] ? Kr[i * PK + ord[i * OP]] : 0ull;
   }
   double wsum = 0.0;
   for (int round = 0; round < N; round++) {
@@ -745,12 +775,12 @@ __device__ __forceinline__ double p2_rounds_keys(const unsigned long long *Kr, i
     for (int cc = 0; cc < KB; cc++) {
       if (lane + 32 * cc == brow) act[cc] = false;
       adv[cc] = act[cc] && 63 - (int)(hk[cc] & 63ull) == bcol;
-      col[cc] = adv[cc] ? (int)ord[(lane + 32 * cc) * N + (++ptr[cc])] : 0;
+      col[cc] = adv[cc] ? (int)ord[(lane + 32 * cc) * OP + (++ptr[cc])] : 0;
     }
 #pragma unroll
     for (int cc = 0; cc < KB; cc++)
       if (adv[cc])
-        while (taken_col(col[cc])) col[cc] = ord[(lane + 32 * cc) * N + (++ptr[cc])];
+        while (taken_col(col[cc])) col[cc] = ord[(lane + 32 * cc) * OP + (++ptr[cc])];
 #pragma unroll
     for (int cc = 0; cc < KB; cc++)
       if (adv[cc]) hk[cc] = Kr[(lane + 32 * cc) * PK + col[cc]];
@@ -973,8 +1003,11 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       // chain over k in order (bitwise equal to the scalar chain, probed on
       // B200: tools/probes/dmma_probe.cu), so X is the same as the m-ascending
       // fma accumulation of the low-rank kernel.  Warp tile grid WR x WC,
-      // TR x TC 8x8 tiles per warp.
-      constexpr int WR = 2, WC = PW / 2, TR = (KB == 1) ? 2 : 4, TC = 4;
+      // TR x TC 8x8 tiles per warp covering BC x BC tiles (N <= 8 BC: the
+      // host launches the BC = 6 instance for N <= 48, so the mma work there
+      // is 36 tiles instead of 64; predicated mma.sync measured slower).
+      constexpr int WR = 2, WC = PW / 2, TR = BC / WR, TC = BC / WC;
+      static_assert(TR * WR == BC && TC * WC == BC && 8 * BC <= 32 * KB, "tile grid");
       const int wr = warp % WR, wc = warp / WR;
       const int lr = lane >> 2, lk = lane & 3;
       double acc[TR][TC][2];
@@ -1062,12 +1095,12 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
       if constexpr (KB == 2) {  // two adjacent lanes per row
         const int row = tid >> 1, half = tid & 1;
         const bool act = row < N;
-        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * N, half, act);
+        p2_row_order_pair<T>(Kr + (act ? row : 0) * PK, N, ord + (act ? row : 0) * p2_ord_pitch(N), half, act);
       } else {
-        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * N);
+        if (tid < N) p2_row_order<T, KB>(Kr + tid * PK, N, ord + tid * p2_ord_pitch(N));
       }
     } else {
-      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * N, lane);
+      for (int i = warp; i < N; i += PW) p2_sort_row<T, KB>(Xs + i * P, N, ord + i * p2_ord_pitch(N), lane);
     }
     if (tid == 0) {
       meta[s].slot = slot;

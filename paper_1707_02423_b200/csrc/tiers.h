@@ -53,7 +53,8 @@
 // two-stage pair kernels: (T, KB, AR, BC, producer warps, MINB)
 #define CFGSIM_P2_LIST(X) \
   X(double, 1, 4, 4, 2, 4) X(double, 2, 4, 8, 4, 2) X(float, 1, 4, 4, 2, 4) X(float, 2, 4, 8, 4, 2) \
-  X(double, 2, 4, 8, 4, 3) X(float, 2, 4, 8, 4, 3) X(double, 1, 4, 4, 2, 6) X(float, 1, 4, 4, 2, 6)
+  X(double, 2, 4, 8, 4, 3) X(float, 2, 4, 8, 4, 3) X(double, 1, 4, 4, 2, 6) X(float, 1, 4, 4, 2, 6) \
+  X(double, 2, 4, 6, 4, 3) X(float, 2, 4, 6, 4, 3)
 #define CFGSIM_EXTERN_P2(T, KB, AR, BC, PW, MINB)                                                   \
   extern template __global__ void cfgsim::isorank_pair2_kernel<T, KB, AR, BC, PW, MINB>(           \
       const int32_t *, cfgsim::PairWork, cfgsim::PairOut, cfgsim::Pair2Params, const T *, const double *, \
