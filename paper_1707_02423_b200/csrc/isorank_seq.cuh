@@ -854,11 +854,16 @@ __global__ void __launch_bounds__(32 * (PW + 1), MINB)
   const int SPD = p2_stage_pitch(NPt, (int)sizeof(T));  // staged row pitch (conflict-free fragment loads)
   unsigned long long ph_t = 0;
   int ph_last = -1;
+  // items are claimed one pair ahead (thread 0 holds the claim in a register
+  // while the current pair runs), so the global atomic's round trip is not
+  // on the producers' path; every claimed item below n_items is processed
+  unsigned long long claim = tid == 0 ? atomicAdd(counter, 1ull) : 0ull;
   for (int it = 0;; it++) {
     const int s = it & 1;
     P2_PHASE(0);  // claim an item + wait for the free buffer
     if (tid == 0) {
-      *s_item = (int64_t)atomicAdd(counter, 1ull);
+      *s_item = (int64_t)claim;
+      claim = atomicAdd(counter, 1ull);
       s_first[0] = 0x7fffffff;
       s_first[1] = 0x7fffffff;
       s_first[2] = -1;
