@@ -117,3 +117,14 @@ def test_native_csv_writer_byte_identical():
     g = load_golden("bundled_corpus.npz")
     pm = P.PairwiseMatrix(P.MeasureId.ISO, tuple(str(x) for x in g["ids"]), g["scores"])
     assert P.export_heatmap_csv(pm, native=True) == (GOLDEN / "iso.csv").read_text()
+
+
+def test_corpus_data_pointers():
+    """DeviceCorpus reads ndarray data addresses from the array objects
+    (corpus._data_pointers); they must equal numpy's own, views included."""
+    import numpy as np
+    from paper_1707_02423_b200.corpus import _data_pointers
+    base = np.arange(64.0).reshape(8, 8)
+    arrs = [np.zeros((3, 3)), base[2:5, 2:5].copy(), np.ascontiguousarray(base[1:]), base[4:], np.ones((1, 1))]
+    assert _data_pointers(arrs) == [a.__array_interface__["data"][0] for a in arrs]
+    assert _data_pointers([]) == []
