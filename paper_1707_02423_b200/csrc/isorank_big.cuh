@@ -331,6 +331,16 @@ __device__ __forceinline__ int big_key_col(unsigned long long k) {
   return (1 << BIG_CB) - 1 - (int)(k & ((1ull << BIG_CB) - 1));
 }
 
+// greedy rounds: entries prefetched to L2 ahead of a row's register window
+#ifndef CFGSIM_BIG_L2_AHEAD
+constexpr int BIG_L2_AHEAD = 16;
+#else
+constexpr int BIG_L2_AHEAD = CFGSIM_BIG_L2_AHEAD;
+#endif
+__device__ __forceinline__ void big_prefetch_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 __device__ __forceinline__ void big_cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // B-byte async copy global -> shared; zero-fills the destination when !valid
@@ -1072,6 +1082,10 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
                 qv[r][f] = sval[(size_t)i * N + 1 + f];
                 qc[r][f] = scol[(size_t)i * N + 1 + f];
               }
+            if (KB <= 16) {
+              for (int e = 1 + PF; e < 1 + PF + BIG_L2_AHEAD && e < N; e += 16) big_prefetch_l2(sval + (size_t)i * N + e);
+              if (1 + PF < N) big_prefetch_l2(scol + (size_t)i * N + 1 + PF);
+            }
           }
         }
         __syncthreads();
@@ -1148,6 +1162,15 @@ __global__ void __launch_bounds__(BIG_THREADS, 2)
                 }
               } while (hc[r] == bcol || ((tk_cur[hc[r] >> 5] >> (hc[r] & 31)) & 1u));
               ptr[r] = p;
+              // keep the row's coming entries in L2: later window refills
+              // and skips past the window then wait on L2, not HBM (the
+              // slabs of all resident CTAs do not stay in L2 on their own).
+              // N <= 512 only: measured +6.7% on a C5 subset, -4% at
+              // N <= 1024 (C4), where 4 rows per thread prefetch 4x the lines
+              if (KB <= 16 && p + PF + BIG_L2_AHEAD < N) {
+                big_prefetch_l2(sval + (size_t)i * N + p + PF + BIG_L2_AHEAD);
+                big_prefetch_l2(scol + (size_t)i * N + p + PF + BIG_L2_AHEAD);
+              }
               adv_steps += (unsigned)(p - p0);  // diagnostics (registers; one atomic per pair)
               adv_deep += (p - p0 > PF) ? 1u : 0u;
             }
